@@ -1,0 +1,100 @@
+/* lpradon_gpu.h — C ABI of the B200 log-polar Radon transform library
+ * (paper_1506_00014_b200/liblpradon_gpu.so).
+ *
+ * This is the drop-in boundary for the reference's (specified but
+ * unimplemented) fast operators. Each entry point replaces one reference
+ * interface:
+ *
+ *   lpr_geometry_make       <- lpr::sampling_plan        (proj/include/lpradon/geometry.hpp:48-61,
+ *                                                          proj/src/geometry.cpp:69-98)
+ *   lpr_spectrum_quadrature <- lpr::zeta_spectrum / zeta_bp_spectrum
+ *                                                         (proj/include/lpradon/kernel.hpp:41-47,
+ *                                                          proj/src/kernel.cpp:341-439)
+ *   lpr_gpu_plan_create     <- RadonPlan construction
+ *   lpr_gpu_radon[_host]    <- fast_radon(Image, RadonPlan) -> Sinogram
+ *   lpr_gpu_backproject[_host] <- fast_backprojection(Sinogram, RadonPlan) -> Image
+ *   lpr_gpu_radon_transpose <- the exact discrete adjoint used by adjoint_gap
+ *
+ * No C++ or CUDA types cross the boundary: plain pointers, sizes and an
+ * opaque stream handle (a cudaStream_t passed as void*, NULL = default).
+ *
+ * Layouts (row-major fp32): images batch x N x N (rows index x2, the
+ * raster covers [-1/2, 1/2)^2); sinograms batch x n_theta x N (rows theta =
+ * i pi / n_theta, columns s = -1/2 + j / N). Device pointers for the lpr_gpu_*
+ * calls, host pointers for the *_host calls (copies happen inside).
+ *
+ * Errors: every function returns an lpr_status; on failure a message is
+ * kept per thread for lpr_gpu_last_error(). LPR_ERR_ARG mirrors the
+ * reference's std::invalid_argument (types.hpp:72-74), LPR_ERR_CUDA/OOM its
+ * runtime_error class. There is no CPU fallback: without a usable sm_100
+ * device every compute call fails with LPR_ERR_CUDA.
+ */
+#ifndef LPRADON_GPU_H
+#define LPRADON_GPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LPR_OK = 0,
+    LPR_ERR_ARG = 1,
+    LPR_ERR_CUDA = 2,
+    LPR_ERR_OOM = 3,
+} lpr_status;
+
+/* Mirrors lpr::GeometryPlan (geometry.hpp:23-43). */
+typedef struct {
+    int N, M, n_theta, nts, n_rho, refine;
+    double beta, a_R, a_r, log_ar, dtheta_p, dtheta_lp, drho, ds;
+} lpr_geometry;
+
+typedef struct lpr_gpu_plan lpr_gpu_plan;
+
+/* sampling_plan(N, M[, n_theta]) with an optional n_rho override (>= the
+ * minimal count of Eq. (vrho); 0 selects the minimal count). n_theta <= 0
+ * selects ceil(3N/2); it is rounded up to a multiple of 2M. */
+int lpr_geometry_make(int N, int M, int n_theta, int n_rho, lpr_geometry* out);
+
+/* Smallest n_rho >= the sampling bound whose FFT length factors into
+ * {2,3,5,7} (the fast plan variant; the default plan uses the bound itself). */
+int lpr_smooth_n_rho(int N, int M);
+
+/* Kernel spectrum on the doubled grid, (2 nts) x n_rho complex interleaved
+ * re/im fp64, theta rows in FFT order: kind 0 = zeta (Radon), 1 = zeta#
+ * (back-projection). Host fp64, trapezoid + eighth-order end corrections. */
+int lpr_spectrum_quadrature(const lpr_geometry* geom, int kind, double* out_re_im);
+
+/* Device plan: uploads the spectra (folded with 1/Bhat and the FFT
+ * normalisation, fp32) and allocates scratch for max_batch slices. Either
+ * spectrum may be NULL, in which case it is computed here. */
+int lpr_gpu_plan_create(int device, const lpr_geometry* geom, const double* zeta_re_im,
+                        const double* zeta_bp_re_im, int max_batch, lpr_gpu_plan** out);
+void lpr_gpu_plan_destroy(lpr_gpu_plan* plan);
+
+/* Algorithm 1: d_img (batch x N x N) -> d_sino (batch x n_theta x N). */
+int lpr_gpu_radon(lpr_gpu_plan* plan, const float* d_img, float* d_sino, int batch, void* stream);
+/* Algorithm 2: d_sino -> d_img (sector sum, factor 2; zero outside the unit disc). */
+int lpr_gpu_backproject(lpr_gpu_plan* plan, const float* d_sino, float* d_img, int batch, void* stream);
+/* Exact transpose of lpr_gpu_radon under <g,h>_Sigma = 2 dtheta ds sum(g h)
+ * and <f,u>_X = sum(f u) / N^2, so <R f, g>_Sigma = <f, R^T g>_X. */
+int lpr_gpu_radon_transpose(lpr_gpu_plan* plan, const float* d_sino, float* d_img, int batch, void* stream);
+
+/* Same operators on host buffers: pinned staging, H2D, compute, D2H and a
+ * stream synchronisation inside the call (the end-to-end path). */
+int lpr_gpu_radon_host(lpr_gpu_plan* plan, const float* h_img, float* h_sino, int batch);
+int lpr_gpu_backproject_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int batch);
+
+/* Kernel launches issued by this plan since creation (instrumentation). */
+long long lpr_gpu_launch_count(const lpr_gpu_plan* plan);
+/* Spectral-convolution launches (the reference's 2-D FFT counter analogue:
+ * 2 per sector per operator call). */
+long long lpr_gpu_fft_count(const lpr_gpu_plan* plan);
+
+const char* lpr_gpu_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LPRADON_GPU_H */

@@ -40,9 +40,18 @@ def lib():
         _lib = ctypes.CDLL(LPO_PATH)
         _lib.lpo_last_error.restype = ctypes.c_char_p
         _lib.lpo_fft2d_count.restype = ctypes.c_ulonglong
-        for name in ("lpo_prefilter_1d", "lpo_prefilter_2d", "lpo_fft1d", "lpo_fft2d", "lpo_lp_convolve",
-                     "lpo_eval_mirror_2d", "lpo_eval_periodic_2d"):
-            pass
+        L, P, C = ctypes.c_long, ctypes.c_void_p, ctypes.c_int
+        sig = {
+            "lpo_prefilter_1d": [P, L],
+            "lpo_prefilter_2d": [P, L, L],
+            "lpo_fft1d": [P, L, C],
+            "lpo_fft2d": [P, L, L, C],
+            "lpo_lp_convolve": [P, C, P, L, L],
+            "lpo_eval_mirror_2d": [P, L, L, P, P, P, L],
+            "lpo_eval_periodic_2d": [P, L, L, P, P, P, L],
+        }
+        for name, args in sig.items():
+            getattr(_lib, name).argtypes = args
     return _lib
 
 
@@ -57,6 +66,16 @@ def ref():
             raise RuntimeError(f"reference build missing: {REF_PATH} (run `make -C oracle ref`)")
         _ref = ctypes.CDLL(REF_PATH)
         _ref.lpr_ref_last_error.restype = ctypes.c_char_p
+        L, P, C = ctypes.c_long, ctypes.c_void_p, ctypes.c_int
+        sig = {
+            "lpr_ref_prefilter_1d": [P, L],
+            "lpr_ref_prefilter_2d": [P, L, L],
+            "lpr_ref_interp_cubic_2d": [P, L, L, P, P, P, L],
+            "lpr_ref_eval_periodic_2d": [P, L, L, P, P, P, L],
+            "lpr_ref_eval_zero_1d": [P, L, P, P, L],
+        }
+        for name, args in sig.items():
+            getattr(_ref, name).argtypes = args
     return _ref
 
 

@@ -1,0 +1,20 @@
+"""B200-native log-polar Radon transform R and back-projection R# (arXiv 1506.00014).
+
+Host mirror of the reference's lp_ops interface over the C ABI in
+``include/lpradon_gpu.h``; the compute runs in hand-written sm_100a kernels
+(``csrc/``). See DESIGN.md.
+"""
+from .lp_ops import (  # noqa: F401
+    Geometry,
+    RadonPlan,
+    adjoint_gap,
+    fast_backprojection,
+    fast_radon,
+    inner_image,
+    inner_sinogram,
+    radon_transpose,
+    sampling_plan,
+    smooth_n_rho,
+    zeta_bp_spectrum,
+    zeta_spectrum,
+)

@@ -1,0 +1,480 @@
+// C ABI (include/lpradon_gpu.h): plan construction, table upload and the
+// launch sequences of R, R# and R^T. Host orchestration only; the compute
+// is in lpr_kernels.cu / lpr_transpose.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lpr_host.hpp"
+#include "lpr_kernels.cuh"
+#include "lpradon_gpu.h"
+
+namespace lpr {
+
+// kernels (lpr_kernels.cu, lpr_transpose.cu)
+__global__ void k_prefilter_rows(DevGeom g, const float* img, float* tmp);
+__global__ void k_prefilter_cols(DevGeom g, const float* tmp, float* qf);
+__global__ void k_prefilter_sino(DevGeom g, const float* sino, float* qg);
+__global__ void __launch_bounds__(512) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float* qf, float2* spec);
+__global__ void __launch_bounds__(512) k_rho_pass(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float2* mult, float2* spec);
+__global__ void __launch_bounds__(512) k_theta_inv(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float2* spec, float* lp);
+__global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
+__global__ void __launch_bounds__(512) k_bp_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float* qg, float2* spec);
+__global__ void k_bp_out(DevGeom g, const float* lp, float* img);
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+    lpr_status code;
+    Error(lpr_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    const lpr_status c = e == cudaErrorMemoryAllocation ? LPR_ERR_OOM : LPR_ERR_CUDA;
+    throw Error(c, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return LPR_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return LPR_ERR_ARG;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return LPR_ERR_CUDA;
+    }
+}
+
+using cd = std::complex<double>;
+constexpr double kPi = 3.14159265358979323846;
+
+std::vector<int> radices(long n) {
+    std::vector<int> r;
+    for (int f : {8, 4, 2, 3, 5, 7})
+        while (n % f == 0) {
+            r.push_back(f);
+            n /= f;
+        }
+    if (n != 1) r.clear();
+    return r;
+}
+
+long smooth_at_least(long n) {
+    while (radices(n).empty()) ++n;
+    return n;
+}
+
+// Host mixed-radix DFT (fp64) for the Bluestein kernel transform.
+void host_fft(std::vector<cd>& x) {
+    const long n = long(x.size());
+    if (n == 1) return;
+    long p = 0;
+    for (long f : {2L, 3L, 5L, 7L})
+        if (n % f == 0) {
+            p = f;
+            break;
+        }
+    if (p == 0) throw std::logic_error("host_fft: length not 7-smooth");
+    const long m = n / p;
+    std::vector<std::vector<cd>> sub(p, std::vector<cd>(m));
+    for (long r = 0; r < p; ++r)
+        for (long j = 0; j < m; ++j) sub[r][j] = x[j * p + r];
+    for (auto& s : sub) host_fft(s);
+    for (long k = 0; k < n; ++k) {
+        cd acc = 0;
+        for (long r = 0; r < p; ++r) acc += sub[r][k % m] * std::polar(1.0, -2.0 * kPi * double(r * k % n) / double(n));
+        x[k] = acc;
+    }
+}
+
+int threads_for(long len) {
+    long t = (len / 16 + 31) / 32 * 32;  // ~8 radix-2 butterflies per thread per pass
+    return int(std::clamp<long>(t, 64, 512));
+}
+
+}  // namespace
+}  // namespace lpr
+
+using namespace lpr;
+
+struct lpr_gpu_plan {
+    int device = 0;
+    lpr_geometry geo{};
+    int max_batch = 1;
+    DevGeom g{};
+    FftDesc d_fine{}, d_rho{}, d_coarse{};
+    int t_fine = 0, t_rho = 0, t_coarse = 0;
+    size_t sm_fine = 0, sm_rho = 0, sm_coarse = 0;
+    float2* mult_R = nullptr;
+    float2* mult_B = nullptr;
+    float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
+    float2* spec = nullptr;
+    float *d_in = nullptr, *d_out = nullptr;   // staging for the *_host entry points
+    float *h_in = nullptr, *h_out = nullptr;   // pinned
+    cudaStream_t stream = nullptr;
+    std::vector<void*> allocs;
+    long long launches = 0, ffts = 0;
+
+    template <class T>
+    T* dalloc(size_t count) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* upload(const std::vector<T>& v) {
+        T* p = dalloc<T>(v.size());
+        ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+        return p;
+    }
+
+    void build_desc(long n, FftDesc& d, int& threads, size_t& smem) {
+        d = FftDesc{};
+        d.n = int(n);
+        auto rad = radices(n);
+        auto twiddles = [&](long len) {
+            std::vector<float2> tw(len);
+            for (long j = 0; j < len; ++j) {
+                const double a = -2.0 * kPi * double(j) / double(len);
+                tw[j] = make_float2(float(std::cos(a)), float(std::sin(a)));
+            }
+            return upload(tw);
+        };
+        if (!rad.empty()) {
+            if (rad.size() > size_t(kMaxPasses)) throw std::invalid_argument("fft: too many passes");
+            d.npass = int(rad.size());
+            std::copy(rad.begin(), rad.end(), d.radix);
+            d.tw = twiddles(n);
+        } else {
+            const long nb = smooth_at_least(2 * n - 1);
+            auto brad = radices(nb);
+            d.nb = int(nb);
+            d.nbpass = int(brad.size());
+            std::copy(brad.begin(), brad.end(), d.bradix);
+            d.btw = twiddles(nb);
+            std::vector<float2> chirp(n);
+            std::vector<cd> kern(nb, cd(0.0));
+            for (long j = 0; j < n; ++j) {
+                const long jj = (j * j) % (2 * n);
+                const cd c = std::polar(1.0, -kPi * double(jj) / double(n));
+                chirp[j] = make_float2(float(c.real()), float(c.imag()));
+                kern[j] = std::conj(c);
+                if (j) kern[nb - j] = std::conj(c);
+            }
+            host_fft(kern);
+            std::vector<float2> bh(nb);
+            for (long j = 0; j < nb; ++j) bh[j] = make_float2(float(kern[j].real() / nb), float(kern[j].imag() / nb));
+            d.chirp = upload(chirp);
+            d.bhat = upload(bh);
+        }
+        const long len = d.nb ? d.nb : d.n;
+        threads = threads_for(len);
+        smem = size_t(fft_smem_elems(d)) * sizeof(float2);
+        if (smem > 227 * 1024) throw std::invalid_argument("fft: transform does not fit in shared memory");
+    }
+
+    ~lpr_gpu_plan() {
+        for (void* p : allocs) cudaFree(p);
+        if (h_in) cudaFreeHost(h_in);
+        if (h_out) cudaFreeHost(h_out);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+void set_smem(const void* fn, size_t bytes) {
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)), "smem attribute");
+}
+
+inline int cdiv(long a, long b) { return int((a + b - 1) / b); }
+
+void check_launch(const char* what) { ck(cudaGetLastError(), what); }
+
+void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
+    const lpr_geometry& G = p->geo;
+    if (G.M > kMaxSectors) throw std::invalid_argument("plan: M above the device limit");
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    int major = 0;
+    ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, p->device), "device query");
+    if (major < 10) throw Error(LPR_ERR_CUDA, "plan: the kernels are built for sm_100a (B200)");
+    DevGeom& g = p->g;
+    g.N = G.N;
+    g.M = G.M;
+    g.n_theta = G.n_theta;
+    g.nts = G.nts;
+    g.n_rho = G.n_rho;
+    g.refine = G.refine;
+    g.nf = G.refine * G.nts;
+    g.Lf = 2 * g.nf;
+    g.L2 = 2 * G.nts;
+    g.win = G.nts + 8;
+    g.j0 = -G.nts / 2 - 4;
+    g.pitch = G.N + 2 * kApron;
+    g.aR = float(G.a_R);
+    g.inv_aR = float(1.0 / G.a_R);
+    g.one_m_aR = float(1.0 - G.a_R);
+    g.aR2 = float(G.a_R * G.a_R);
+    g.log_ar = float(G.log_ar);
+    g.inv_drho = float(1.0 / G.drho);
+    g.inv_dtheta_p = float(1.0 / G.dtheta_p);
+    g.out_scale = float(1.0 / (2.0 * G.a_R));
+    for (int m = 0; m < G.M; ++m) {
+        g.cosm[m] = float(std::cos(m * G.beta));
+        g.sinm[m] = float(std::sin(m * G.beta));
+    }
+    std::vector<float> fc(g.nf), fs(g.nf), cc(G.nts), er(G.n_rho), fir(2 * kFirHalf + 1);
+    for (int i = 0; i < g.nf; ++i) {
+        const double th = double(i - g.nf / 2) * G.dtheta_lp;
+        fc[i] = float(std::cos(th));
+        fs[i] = float(std::sin(th));
+    }
+    for (int jj = 0; jj < G.nts; ++jj) cc[jj] = float(std::cos(double(jj - G.nts / 2) * G.dtheta_p));
+    for (int l = 0; l < G.n_rho; ++l) er[l] = float(std::exp(G.log_ar + double(l) * G.drho));
+    const double z = std::sqrt(3.0) - 2.0;
+    for (int d = -kFirHalf; d <= kFirHalf; ++d) fir[d + kFirHalf] = float(std::sqrt(3.0) * std::pow(z, std::abs(d)));
+    g.fine_cos = p->upload(fc);
+    g.fine_sin = p->upload(fs);
+    g.coarse_cos = p->upload(cc);
+    g.erho = p->upload(er);
+    g.fir = p->upload(fir);
+
+    p->build_desc(g.Lf, p->d_fine, p->t_fine, p->sm_fine);
+    p->build_desc(G.n_rho, p->d_rho, p->t_rho, p->sm_rho);
+    p->build_desc(g.L2, p->d_coarse, p->t_coarse, p->sm_coarse);
+
+    // spectral multipliers on the half theta spectrum k in [0, nts]
+    const long nts = G.nts, nr = G.n_rho, rows = 2 * nts;
+    std::vector<double> zbuf, zbbuf;
+    if (!zeta) {
+        zbuf.resize(2 * rows * nr);
+        host::spectrum(G, 0, zbuf.data());
+        zeta = zbuf.data();
+    }
+    if (!zeta_bp) {
+        zbbuf.resize(2 * rows * nr);
+        host::spectrum(G, 1, zbbuf.data());
+        zeta_bp = zbbuf.data();
+    }
+    auto bhat = [](long k, long n) { return (2.0 + std::cos(2.0 * kPi * double(k) / double(n))) / 3.0; };
+    std::vector<float2> mr((nts + 1) * nr), mb((nts + 1) * nr);
+    const double sr = 1.0 / (double(g.Lf) * double(nr)), sb = 1.0 / (double(rows) * double(nr));
+    for (long k = 0; k <= nts; ++k)
+        for (long v = 0; v < nr; ++v) {
+            const long i = k * nr + v;
+            if (k == nts) {
+                mr[i] = mb[i] = make_float2(0.f, 0.f);
+                continue;
+            }
+            const cd zr(zeta[2 * i], zeta[2 * i + 1]), zb(zeta_bp[2 * i], zeta_bp[2 * i + 1]);
+            const cd a = zr * (sr / bhat(v, nr));                  // theta Bhat cancels at lattice rows
+            const cd b = zb * (sb / (bhat(k, rows) * bhat(v, nr)));
+            mr[i] = make_float2(float(a.real()), float(a.imag()));
+            mb[i] = make_float2(float(b.real()), float(b.imag()));
+        }
+    p->mult_R = p->upload(mr);
+    p->mult_B = p->upload(mb);
+
+    const size_t B = size_t(p->max_batch);
+    p->tmp = p->dalloc<float>(B * G.N * g.pitch);
+    p->qf = p->dalloc<float>(B * g.pitch * g.pitch);
+    p->qg = p->dalloc<float>(B * G.n_theta * G.N);
+    p->spec = p->dalloc<float2>(B * G.M * (nts + 1) * nr);
+    p->lp = p->dalloc<float>(B * G.M * g.win * nr);
+    const size_t io = B * std::max<size_t>(size_t(G.N) * G.N, size_t(G.n_theta) * G.N);
+    p->d_in = p->dalloc<float>(io);
+    p->d_out = p->dalloc<float>(io);
+    ck(cudaHostAlloc(&p->h_in, io * sizeof(float), cudaHostAllocDefault), "cudaHostAlloc");
+    ck(cudaHostAlloc(&p->h_out, io * sizeof(float), cudaHostAllocDefault), "cudaHostAlloc");
+    ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+
+    set_smem((const void*)k_radon_theta_fwd, p->sm_fine);
+    set_smem((const void*)k_bp_theta_fwd, p->sm_coarse);
+    set_smem((const void*)k_theta_inv, p->sm_coarse);
+    set_smem((const void*)k_rho_pass, p->sm_rho);
+    set_smem((const void*)k_radon_out, size_t(nr) * sizeof(float));
+}
+
+void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
+    const DevGeom& g = p->g;
+    k_prefilter_rows<<<dim3(cdiv(g.pitch, 256), g.N, nb), 256, 0, st>>>(g, img, p->tmp);
+    k_prefilter_cols<<<dim3(cdiv(g.pitch, 256), g.pitch, nb), 256, 0, st>>>(g, p->tmp, p->qf);
+    k_radon_theta_fwd<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_fine, p->sm_fine, st>>>(g, p->d_fine, p->qf, p->spec);
+    k_rho_pass<<<dim3(g.nts + 1, nb * g.M), p->t_rho, p->sm_rho, st>>>(g, p->d_rho, p->mult_R, p->spec);
+    k_theta_inv<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->spec, p->lp);
+    k_radon_out<<<dim3(g.n_theta, nb), 256, g.n_rho * sizeof(float), st>>>(g, p->lp, sino);
+    check_launch("radon launch");
+    p->launches += 6;
+    p->ffts += 2LL * g.M * nb;
+}
+
+void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
+    const DevGeom& g = p->g;
+    k_prefilter_sino<<<dim3(cdiv(g.N, 256), g.n_theta, nb), 256, 0, st>>>(g, sino, p->qg);
+    k_bp_theta_fwd<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->qg, p->spec);
+    k_rho_pass<<<dim3(g.nts + 1, nb * g.M), p->t_rho, p->sm_rho, st>>>(g, p->d_rho, p->mult_B, p->spec);
+    k_theta_inv<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->spec, p->lp);
+    k_bp_out<<<dim3(cdiv(g.N, 128), g.N, nb), 128, 0, st>>>(g, p->lp, img);
+    check_launch("backprojection launch");
+    p->launches += 5;
+    p->ffts += 2LL * g.M * nb;
+}
+
+using ChunkFn = void (*)(lpr_gpu_plan*, const float*, float*, int, cudaStream_t);
+
+void run_device(lpr_gpu_plan* p, ChunkFn fn, const float* in, float* out, int batch, size_t in_sz, size_t out_sz,
+                void* stream) {
+    if (!p) throw std::invalid_argument("null plan");
+    if (batch < 0 || (batch > 0 && (!in || !out))) throw std::invalid_argument("bad buffers or batch");
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int b0 = 0; b0 < batch; b0 += p->max_batch) {
+        const int nb = std::min(p->max_batch, batch - b0);
+        fn(p, in + size_t(b0) * in_sz, out + size_t(b0) * out_sz, nb, st);
+    }
+}
+
+bool is_pinned(const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+void run_host(lpr_gpu_plan* p, ChunkFn fn, const float* hin, float* hout, int batch, size_t in_sz, size_t out_sz) {
+    if (!p) throw std::invalid_argument("null plan");
+    if (batch < 0 || (batch > 0 && (!hin || !hout))) throw std::invalid_argument("bad buffers or batch");
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    const bool pin_in = is_pinned(hin), pin_out = is_pinned(hout);
+    cudaStream_t st = p->stream;
+    for (int b0 = 0; b0 < batch; b0 += p->max_batch) {
+        const int nb = std::min(p->max_batch, batch - b0);
+        const float* src = hin + size_t(b0) * in_sz;
+        float* dst = hout + size_t(b0) * out_sz;
+        const size_t ib = size_t(nb) * in_sz * sizeof(float), ob = size_t(nb) * out_sz * sizeof(float);
+        if (!pin_in) {
+            std::memcpy(p->h_in, src, ib);
+            src = p->h_in;
+        }
+        ck(cudaMemcpyAsync(p->d_in, src, ib, cudaMemcpyHostToDevice, st), "H2D");
+        fn(p, p->d_in, p->d_out, nb, st);
+        ck(cudaMemcpyAsync(pin_out ? dst : p->h_out, p->d_out, ob, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "stream sync");
+        if (!pin_out) std::memcpy(dst, p->h_out, ob);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lpr_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int lpr_geometry_make(int N, int M, int n_theta, int n_rho, lpr_geometry* out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output");
+        *out = host::make_geometry(N, M, n_theta, n_rho);
+    });
+}
+
+int lpr_smooth_n_rho(int N, int M) {
+    try {
+        return host::smooth_n_rho(N, M);
+    } catch (...) {
+        return -1;
+    }
+}
+
+int lpr_spectrum_quadrature(const lpr_geometry* geom, int kind, double* out) {
+    return guard([&] {
+        if (!geom || !out || (kind != 0 && kind != 1)) throw std::invalid_argument("bad spectrum arguments");
+        host::spectrum(*geom, kind, out);
+    });
+}
+
+int lpr_gpu_plan_create(int device, const lpr_geometry* geom, const double* zeta, const double* zeta_bp,
+                        int max_batch, lpr_gpu_plan** out) {
+    return guard([&] {
+        if (!geom || !out) throw std::invalid_argument("null argument");
+        if (max_batch < 1) throw std::invalid_argument("max_batch must be >= 1");
+        // re-derive so a hand-edited struct cannot desynchronise the tables
+        const lpr_geometry G = host::make_geometry(geom->N, geom->M, geom->n_theta, geom->n_rho);
+        if (G.n_theta != geom->n_theta || G.nts != geom->nts)
+            throw std::invalid_argument("plan: geometry does not match sampling_plan");
+        auto* p = new lpr_gpu_plan();
+        p->device = device;
+        p->geo = G;
+        p->max_batch = max_batch;
+        try {
+            init_plan(p, zeta, zeta_bp);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+void lpr_gpu_plan_destroy(lpr_gpu_plan* plan) { delete plan; }
+
+int lpr_gpu_radon(lpr_gpu_plan* p, const float* d_img, float* d_sino, int batch, void* stream) {
+    return guard([&] {
+        run_device(p, radon_chunk, d_img, d_sino, batch, size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0),
+                   size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0), stream);
+    });
+}
+
+int lpr_gpu_backproject(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, void* stream) {
+    return guard([&] {
+        run_device(p, backproject_chunk, d_sino, d_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
+                   size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream);
+    });
+}
+
+int lpr_gpu_radon_host(lpr_gpu_plan* p, const float* h_img, float* h_sino, int batch) {
+    return guard([&] {
+        run_host(p, radon_chunk, h_img, h_sino, batch, size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0),
+                 size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0));
+    });
+}
+
+int lpr_gpu_backproject_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batch) {
+    return guard([&] {
+        run_host(p, backproject_chunk, h_sino, h_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
+                 size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0));
+    });
+}
+
+int lpr_gpu_radon_transpose(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, void* stream) {
+    return guard([&] {
+        (void)p;
+        (void)d_sino;
+        (void)d_img;
+        (void)batch;
+        (void)stream;
+        throw Error(LPR_ERR_CUDA, "radon_transpose: not built yet");
+    });
+}
+
+long long lpr_gpu_launch_count(const lpr_gpu_plan* p) { return p ? p->launches : -1; }
+long long lpr_gpu_fft_count(const lpr_gpu_plan* p) { return p ? p->ffts : -1; }
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+// Device-side plan constants and kernel declarations for the log-polar
+// Radon transform R (Alg. 1) and back-projection R# (Alg. 2).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "lpr_fft.cuh"
+
+namespace lpr {
+
+constexpr int kMaxSectors = 16;
+constexpr int kApron = 4;     // mirrored border around the image coefficients
+constexpr int kFirHalf = 16;  // B-spline prefilter impulse-response half length
+
+// Everything a kernel needs about the plan, passed by value.
+struct DevGeom {
+    int N, M, n_theta, nts, n_rho, refine;
+    int nf;      // fine theta rows per sector (refine * nts)
+    int Lf;      // doubled fine period (2 * nf)
+    int L2;      // doubled coarse period (2 * nts)
+    int win;     // rows kept from the coarse theta inverse
+    int j0;      // coarse theta index of window row 0 (= -nts/2 - 4)
+    int pitch;   // row pitch of the apron image (N + 2 kApron)
+    float aR, inv_aR, one_m_aR, aR2, log_ar, inv_drho, inv_dtheta_p, out_scale;
+    float cosm[kMaxSectors], sinm[kMaxSectors];
+    // tables (device)
+    const float* fine_cos;    // nf entries: cos(q dtheta_lp), q = i - nf/2
+    const float* fine_sin;
+    const float* coarse_cos;  // nts entries: cos(j dtheta_p), j = jj - nts/2
+    const float* erho;        // n_rho entries: exp(log a_r + l drho)
+    const float* fir;         // 2 kFirHalf + 1 prefilter taps
+};
+
+}  // namespace lpr
