@@ -85,6 +85,13 @@ int lpr_gpu_radon_transpose(lpr_gpu_plan* plan, const float* d_sino, float* d_im
 int lpr_gpu_radon_host(lpr_gpu_plan* plan, const float* h_img, float* h_sino, int batch);
 int lpr_gpu_backproject_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int batch);
 
+/* Instrumentation: run one chunk of op (0 = R, 1 = R#) on device buffers
+ * `reps` times on the plan's stream with CUDA events between the launches;
+ * ms[i] is the mean duration of kernel i, names[i] its stage name (static
+ * strings; pass arrays of at least 8). batch <= max_batch. */
+int lpr_gpu_profile_stages(lpr_gpu_plan* plan, int op, const float* d_in, float* d_out, int batch, int reps,
+                           double* ms, int* nstages, const char** names);
+
 /* Kernel launches issued by this plan since creation (instrumentation). */
 long long lpr_gpu_launch_count(const lpr_gpu_plan* plan);
 /* Spectral-convolution launches (the reference's 2-D FFT counter analogue:

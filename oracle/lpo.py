@@ -264,7 +264,7 @@ def smooth_disc_image(N: int, support_radius: float, seed: int, blur_sigma: floa
     edge = 0.85 * r_raster
     w = np.where(rad < edge, 1.0, np.where(rad < r_raster, 0.5 * (1 + np.cos(np.pi * (rad - edge) / (r_raster - edge))), 0.0))
     img *= w
-    return img / np.abs(img).max()
+    return np.ascontiguousarray(img / np.abs(img).max())
 
 
 def rel_l2(a, b) -> float:

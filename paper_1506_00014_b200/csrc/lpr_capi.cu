@@ -127,6 +127,7 @@ struct lpr_gpu_plan {
     float *d_in = nullptr, *d_out = nullptr;   // staging for the *_host entry points
     float *h_in = nullptr, *h_out = nullptr;   // pinned
     cudaStream_t stream = nullptr;
+    cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     std::vector<void*> allocs;
     long long launches = 0, ffts = 0;
 
@@ -311,30 +312,52 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     set_smem((const void*)k_radon_out, size_t(nr) * sizeof(float));
 }
 
+// Optional per-stage profiling: when p->prof is set, an event is recorded
+// before the first and after every launch (lpr_gpu_profile_stages).
+inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
+    if (p->prof) ck(cudaEventRecord(p->prof[i], st), "profile event");
+}
+
 void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
+    mark(p, 0, st);
     k_prefilter_rows<<<dim3(cdiv(g.pitch, 256), g.N, nb), 256, 0, st>>>(g, img, p->tmp);
+    mark(p, 1, st);
     k_prefilter_cols<<<dim3(cdiv(g.pitch, 256), g.pitch, nb), 256, 0, st>>>(g, p->tmp, p->qf);
+    mark(p, 2, st);
     k_radon_theta_fwd<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_fine, p->sm_fine, st>>>(g, p->d_fine, p->qf, p->spec);
+    mark(p, 3, st);
     k_rho_pass<<<dim3(g.nts + 1, nb * g.M), p->t_rho, p->sm_rho, st>>>(g, p->d_rho, p->mult_R, p->spec);
+    mark(p, 4, st);
     k_theta_inv<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->spec, p->lp);
+    mark(p, 5, st);
     k_radon_out<<<dim3(g.n_theta, nb), 256, g.n_rho * sizeof(float), st>>>(g, p->lp, sino);
+    mark(p, 6, st);
     check_launch("radon launch");
     p->launches += 6;
     p->ffts += 2LL * g.M * nb;
 }
+const char* const kRadonStages[] = {"prefilter_rows", "prefilter_cols", "radon_theta_fwd", "rho_pass",
+                                    "theta_inv", "radon_out"};
 
 void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
+    mark(p, 0, st);
     k_prefilter_sino<<<dim3(cdiv(g.N, 256), g.n_theta, nb), 256, 0, st>>>(g, sino, p->qg);
+    mark(p, 1, st);
     k_bp_theta_fwd<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->qg, p->spec);
+    mark(p, 2, st);
     k_rho_pass<<<dim3(g.nts + 1, nb * g.M), p->t_rho, p->sm_rho, st>>>(g, p->d_rho, p->mult_B, p->spec);
+    mark(p, 3, st);
     k_theta_inv<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->spec, p->lp);
+    mark(p, 4, st);
     k_bp_out<<<dim3(cdiv(g.N, 128), g.N, nb), 128, 0, st>>>(g, p->lp, img);
+    mark(p, 5, st);
     check_launch("backprojection launch");
     p->launches += 5;
     p->ffts += 2LL * g.M * nb;
 }
+const char* const kBackprojectStages[] = {"prefilter_sino", "bp_theta_fwd", "rho_pass", "theta_inv", "bp_out"};
 
 using ChunkFn = void (*)(lpr_gpu_plan*, const float*, float*, int, cudaStream_t);
 
@@ -471,6 +494,42 @@ int lpr_gpu_radon_transpose(lpr_gpu_plan* p, const float* d_sino, float* d_img, 
         (void)batch;
         (void)stream;
         throw Error(LPR_ERR_CUDA, "radon_transpose: not built yet");
+    });
+}
+
+int lpr_gpu_profile_stages(lpr_gpu_plan* p, int op, const float* d_in, float* d_out, int batch, int reps,
+                           double* ms, int* nstages, const char** names) {
+    return guard([&] {
+        if (!p || !d_in || !d_out || !ms || !nstages || batch < 1 || batch > p->max_batch || reps < 1)
+            throw std::invalid_argument("profile: bad arguments");
+        if (op != 0 && op != 1) throw std::invalid_argument("profile: op must be 0 (R) or 1 (R#)");
+        ck(cudaSetDevice(p->device), "cudaSetDevice");
+        const int ns = op == 0 ? 6 : 5;
+        std::vector<cudaEvent_t> ev(ns + 1);
+        for (auto& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+        std::vector<double> acc(ns, 0.0);
+        cudaStream_t st = p->stream;
+        for (int r = 0; r < reps; ++r) {
+            p->prof = ev.data();
+            try {
+                (op == 0 ? radon_chunk : backproject_chunk)(p, d_in, d_out, batch, st);
+            } catch (...) {
+                p->prof = nullptr;
+                throw;
+            }
+            p->prof = nullptr;
+            ck(cudaStreamSynchronize(st), "profile sync");
+            for (int i = 0; i < ns; ++i) {
+                float t = 0.f;
+                ck(cudaEventElapsedTime(&t, ev[i], ev[i + 1]), "cudaEventElapsedTime");
+                acc[i] += t;
+            }
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        for (int i = 0; i < ns; ++i) ms[i] = acc[i] / reps;
+        *nstages = ns;
+        if (names)
+            for (int i = 0; i < ns; ++i) names[i] = op == 0 ? kRadonStages[i] : kBackprojectStages[i];
     });
 }
 

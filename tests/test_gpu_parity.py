@@ -1,0 +1,147 @@
+"""GPU parity: the sm_100a path through the C ABI against the fp64 oracle.
+
+Bar (BASELINE.json north_star): relative l2 <= 1e-4 in fp32 for R and R# on
+the same inputs. Inputs are the reference's two synthetic families: the
+modified Shepp-Logan phantom and smooth random discs. Plans cover the
+default sampling_plan (non-smooth N_rho -> Bluestein rho FFT) and the
+7-smooth N_rho variant used for throughput.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _setup(lp, lpo, N, n_rho=0, max_batch=2):
+    g = lp.sampling_plan(N, 3, 0, n_rho)
+    p = lpo.make_plan(N, 3, 0, n_rho)
+    z, zb = lpo.spectrum(p, 0), lpo.spectrum(p, 1)
+    return g, p, z, zb, lp.RadonPlan(g, z, zb, max_batch=max_batch)
+
+
+def _inputs(lpo, N, n):
+    f = np.stack([lpo.smooth_disc_image(N, 0.9, 11 + i) for i in range(n)])
+    f[0] = lpo.phantom_image(N)
+    return f
+
+
+@pytest.mark.parametrize("N,smooth", [(64, False), (128, False), (256, False), (256, True), (512, False),
+                                      (512, True)])
+def test_radon_and_backprojection_parity(lp, lpo, cuda, N, smooth):
+    import torch
+
+    n_rho = lp.smooth_n_rho(N) if smooth else 0
+    g, p, z, zb, plan = _setup(lp, lpo, N, n_rho, max_batch=2)
+    f = _inputs(lpo, N, 3)  # 3 slices through a plan of 2 -> exercises chunking
+    want = lpo.fast_radon(p, z, f)
+    got = lp.fast_radon(torch.tensor(f, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    for i in range(3):
+        assert lpo.rel_l2(got[i], want[i]) <= TOL, (i, lpo.rel_l2(got[i], want[i]))
+    wantb = lpo.fast_backprojection(p, zb, want)
+    gotb = lp.fast_backprojection(torch.tensor(want, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    for i in range(3):
+        assert lpo.rel_l2(gotb[i], wantb[i]) <= TOL, (i, lpo.rel_l2(gotb[i], wantb[i]))
+
+
+def test_random_sinogram_backprojection_parity(lp, lpo, cuda):
+    import torch
+
+    N = 128
+    g, p, z, zb, plan = _setup(lp, lpo, N)
+    rng = np.random.default_rng(3)
+    s = rng.uniform(-1, 1, (g.n_theta, N))
+    want = lpo.fast_backprojection(p, zb, s)
+    got = lp.fast_backprojection(torch.tensor(s, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    assert lpo.rel_l2(got, want) <= TOL
+
+
+@pytest.mark.parametrize("smooth", [False, True])
+def test_parity_n2048(lp, lpo, cuda, smooth):
+    """Config 3 (N=2048, 3072 angles) against the oracle on one slice each way."""
+    import torch
+
+    N = 2048
+    n_rho = lp.smooth_n_rho(N) if smooth else 0
+    g, p, z, zb, plan = _setup(lp, lpo, N, n_rho, max_batch=1)
+    f = lpo.phantom_image(N) if smooth else lpo.smooth_disc_image(N, 0.9, 5)
+    want = lpo.fast_radon(p, z, f)
+    got = lp.fast_radon(torch.tensor(f, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    assert lpo.rel_l2(got, want) <= TOL
+    wantb = lpo.fast_backprojection(p, zb, want)
+    gotb = lp.fast_backprojection(torch.tensor(want, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    assert lpo.rel_l2(gotb, wantb) <= TOL
+
+
+def test_host_entry_points_match_device(lp, lpo, cuda):
+    import torch
+
+    N = 128
+    g, p, z, zb, plan = _setup(lp, lpo, N, max_batch=2)
+    f = _inputs(lpo, N, 3).astype(np.float32)
+    dev = lp.fast_radon(torch.tensor(f, device=cuda), plan).cpu().numpy()
+    host = lp.fast_radon(f, plan)  # numpy -> lpr_gpu_radon_host
+    np.testing.assert_array_equal(dev, host)
+    devb = lp.fast_backprojection(torch.tensor(dev, device=cuda), plan).cpu().numpy()
+    hostb = lp.fast_backprojection(host, plan)
+    np.testing.assert_array_equal(devb, hostb)
+
+
+def test_zero_linearity_and_edge_cases(lp, lpo, cuda):
+    import torch
+
+    N = 64
+    g, p, z, zb, plan = _setup(lp, lpo, N)
+    zero = torch.zeros(N, N, device=cuda)
+    assert not lp.fast_radon(zero, plan).any()
+    assert not lp.fast_backprojection(torch.zeros(g.n_theta, N, device=cuda), plan).any()
+    f1 = torch.tensor(lpo.smooth_disc_image(N, 0.9, 1), dtype=torch.float32, device=cuda)
+    f2 = torch.tensor(lpo.smooth_disc_image(N, 0.9, 2), dtype=torch.float32, device=cuda)
+    lhs = lp.fast_radon(2.5 * f1 - 1.25 * f2, plan)
+    rhs = 2.5 * lp.fast_radon(f1, plan) - 1.25 * lp.fast_radon(f2, plan)
+    assert float((lhs - rhs).norm() / rhs.norm()) <= 1e-5
+    # empty batch is a no-op; wrong shapes raise like std::invalid_argument
+    assert lp.fast_radon(torch.zeros(0, N, N, device=cuda), plan).shape == (0, g.n_theta, N)
+    with pytest.raises(ValueError):
+        lp.fast_radon(torch.zeros(N, N + 2, device=cuda), plan)
+    with pytest.raises(ValueError):
+        lp.fast_backprojection(np.zeros((g.n_theta + 1, N), np.float32), plan)
+    # back-projection is zero outside the unit disc
+    s = torch.rand(g.n_theta, N, device=cuda)
+    img = lp.fast_backprojection(s, plan).cpu().numpy()
+    x = (np.arange(N) * 2 - N)
+    outside = (x[None, :] ** 2 + x[:, None] ** 2) > N * N
+    assert not img[outside].any()
+
+
+def test_adjoint_gap_algorithm2_gpu(lp, lpo, cuda):
+    # gap <= 2e-2 at N=64 over 20 random pairs
+    g, p, z, zb, plan = _setup(lp, lpo, 64)
+    assert lp.adjoint_gap(plan, trials=20) <= 2e-2
+
+
+def test_counters_and_no_cpu_fallback(lp, lpo, cuda):
+    import torch
+
+    g, p, z, zb, plan = _setup(lp, lpo, 64)
+    l0, f0 = plan.launch_count(), plan.fft_count()
+    lp.fast_radon(torch.zeros(3, 64, 64, device=cuda), plan)
+    assert plan.launch_count() > l0
+    assert plan.fft_count() - f0 == 2 * g.M * 3  # 2M spectral transforms per slice
+
+
+def test_sinogram_of_disc_is_rotation_invariant(lp, lpo, cuda):
+    """Size-independent property at N=2048: a centred disc's sinogram is the
+    same on every row and matches 2 sqrt(r^2 - s^2)."""
+    import torch
+
+    N = 2048
+    g = lp.sampling_plan(N, 3, 0, lp.smooth_n_rho(N))
+    plan = lp.RadonPlan(g, max_batch=1)
+    x = (np.arange(N) - N / 2) / N
+    f = (np.hypot(x[None, :], x[:, None]) <= 0.2).astype(np.float32)
+    s = lp.fast_radon(torch.tensor(f, device=cuda), plan).cpu().numpy().astype(np.float64)
+    want = 2 * np.sqrt(np.clip(0.04 - x ** 2, 0, None))
+    assert lpo.rel_l2(s.mean(axis=0), want) <= 5e-3
+    assert np.abs(s - s.mean(axis=0)).max() <= 1e-2 * want.max()
