@@ -18,15 +18,13 @@
 namespace lpr {
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
-__global__ void k_prefilter_rows(DevGeom g, const float* img, float* tmp);
-__global__ void k_prefilter_cols(DevGeom g, const float* tmp, float* qf);
-__global__ void k_prefilter_sino(DevGeom g, const float* sino, float* qg);
-__global__ void __launch_bounds__(512) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float* qf, float2* spec);
-__global__ void __launch_bounds__(512) k_rho_pass(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float2* mult, float2* spec);
-__global__ void __launch_bounds__(512) k_theta_inv(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float2* spec, float* lp);
+__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* img, float* qf);
+__global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* sino, float* qg);
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
-__global__ void __launch_bounds__(512) k_bp_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float* qg, float2* spec);
 __global__ void k_bp_out(DevGeom g, const float* lp, float* img);
+__global__ void k_radon_out_T(DevGeom g, const float* sino, float* lp);
+__global__ void k_prefilter_cols_T(DevGeom g, const float* band, int H, const float* qbar, float* tmp);
+__global__ void k_prefilter_rows_T(DevGeom g, const float* band, int H, const float* tmp, float* img, float scale);
 
 namespace {
 
@@ -102,10 +100,6 @@ void host_fft(std::vector<cd>& x) {
     }
 }
 
-int threads_for(long len) {
-    long t = (len / 16 + 31) / 32 * 32;  // ~8 radix-2 butterflies per thread per pass
-    return int(std::clamp<long>(t, 64, 512));
-}
 
 }  // namespace
 }  // namespace lpr
@@ -118,10 +112,12 @@ struct lpr_gpu_plan {
     int max_batch = 1;
     DevGeom g{};
     FftDesc d_fine{}, d_rho{}, d_coarse{};
-    int t_fine = 0, t_rho = 0, t_coarse = 0;
-    size_t sm_fine = 0, sm_rho = 0, sm_coarse = 0;
+    FftLaunch l_fine{}, l_rho{}, l_coarse{};
     float2* mult_R = nullptr;
     float2* mult_B = nullptr;
+    float2* mult_RT = nullptr;   // conj(mult_R): the transposed rho multiplier
+    float* band = nullptr;       // banded transpose of the apron-extended 1-D prefilter
+    int band_h = 0;
     float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
     float2* spec = nullptr;
     float *d_in = nullptr, *d_out = nullptr;   // staging for the *_host entry points
@@ -145,7 +141,7 @@ struct lpr_gpu_plan {
         return p;
     }
 
-    void build_desc(long n, FftDesc& d, int& threads, size_t& smem) {
+    void build_desc(long n, FftDesc& d, FftLaunch& launch) {
         d = FftDesc{};
         d.n = int(n);
         auto rad = radices(n);
@@ -184,10 +180,8 @@ struct lpr_gpu_plan {
             d.chirp = upload(chirp);
             d.bhat = upload(bh);
         }
-        const long len = d.nb ? d.nb : d.n;
-        threads = threads_for(len);
-        smem = size_t(fft_smem_elems(d)) * sizeof(float2);
-        if (smem > 227 * 1024) throw std::invalid_argument("fft: transform does not fit in shared memory");
+        launch = fft_launch_config(d);
+        if (launch.smem > 227 * 1024) throw std::invalid_argument("fft: transform does not fit in shared memory");
     }
 
     ~lpr_gpu_plan() {
@@ -256,9 +250,9 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     g.erho = p->upload(er);
     g.fir = p->upload(fir);
 
-    p->build_desc(g.Lf, p->d_fine, p->t_fine, p->sm_fine);
-    p->build_desc(G.n_rho, p->d_rho, p->t_rho, p->sm_rho);
-    p->build_desc(g.L2, p->d_coarse, p->t_coarse, p->sm_coarse);
+    p->build_desc(g.Lf, p->d_fine, p->l_fine);
+    p->build_desc(G.n_rho, p->d_rho, p->l_rho);
+    p->build_desc(g.L2, p->d_coarse, p->l_coarse);
 
     // spectral multipliers on the half theta spectrum k in [0, nts]
     const long nts = G.nts, nr = G.n_rho, rows = 2 * nts;
@@ -291,6 +285,36 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         }
     p->mult_R = p->upload(mr);
     p->mult_B = p->upload(mb);
+    for (auto& v : mr) v.y = -v.y;
+    p->mult_RT = p->upload(mr);
+
+    // Q1 (pitch x N): apron-extended FIR prefilter as the forward kernels apply
+    // it (fp32 taps); band[c][j] = Q1[c + A - H + j][c] holds its transpose.
+    {
+        const int N = G.N, pitch = g.pitch, H = kFirHalf + kApron + 8;
+        auto mir = [](int i, int n) {
+            if (n == 1) return 0;
+            const int per = 2 * (n - 1);
+            int r = i % per;
+            if (r < 0) r += per;
+            return r >= n ? per - r : r;
+        };
+        std::vector<double> q1(size_t(pitch) * N, 0.0);
+        for (int cp = 0; cp < pitch; ++cp)
+            for (int d = -kFirHalf; d <= kFirHalf; ++d)
+                q1[size_t(cp) * N + mir(mir(cp - kApron, N) + d, N)] += double(fir[d + kFirHalf]);
+        std::vector<float> band(size_t(N) * (2 * H + 1), 0.f);
+        for (int cp = 0; cp < pitch; ++cp)
+            for (int c = 0; c < N; ++c) {
+                const double v = q1[size_t(cp) * N + c];
+                if (v == 0.0) continue;
+                const int j = cp - (c + kApron - H);
+                if (j < 0 || j > 2 * H) throw std::invalid_argument("plan: prefilter transpose band too narrow for N");
+                band[size_t(c) * (2 * H + 1) + j] = float(v);
+            }
+        p->band = p->upload(band);
+        p->band_h = H;
+    }
 
     const size_t B = size_t(p->max_batch);
     p->tmp = p->dalloc<float>(B * G.N * g.pitch);
@@ -305,11 +329,10 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     ck(cudaHostAlloc(&p->h_out, io * sizeof(float), cudaHostAllocDefault), "cudaHostAlloc");
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
 
-    set_smem((const void*)k_radon_theta_fwd, p->sm_fine);
-    set_smem((const void*)k_bp_theta_fwd, p->sm_coarse);
-    set_smem((const void*)k_theta_inv, p->sm_coarse);
-    set_smem((const void*)k_rho_pass, p->sm_rho);
+    ck(prepare_fft_kernels(p->l_fine, p->l_rho, p->l_coarse), "fft smem attributes");
     set_smem((const void*)k_radon_out, size_t(nr) * sizeof(float));
+    set_smem((const void*)k_radon_out_T, size_t(nr) * sizeof(float));
+
 }
 
 // Optional per-stage profiling: when p->prof is set, an event is recorded
@@ -321,35 +344,32 @@ inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
 void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
     mark(p, 0, st);
-    k_prefilter_rows<<<dim3(cdiv(g.pitch, 256), g.N, nb), 256, 0, st>>>(g, img, p->tmp);
+    k_prefilter_2d<<<dim3(cdiv(g.pitch, 32), cdiv(g.pitch, 32), nb), 256, 0, st>>>(g, img, p->qf);
     mark(p, 1, st);
-    k_prefilter_cols<<<dim3(cdiv(g.pitch, 256), g.pitch, nb), 256, 0, st>>>(g, p->tmp, p->qf);
+    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->qf, p->spec);
     mark(p, 2, st);
-    k_radon_theta_fwd<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_fine, p->sm_fine, st>>>(g, p->d_fine, p->qf, p->spec);
+    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_R, p->spec);
     mark(p, 3, st);
-    k_rho_pass<<<dim3(g.nts + 1, nb * g.M), p->t_rho, p->sm_rho, st>>>(g, p->d_rho, p->mult_R, p->spec);
+    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->spec, p->lp);
     mark(p, 4, st);
-    k_theta_inv<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->spec, p->lp);
-    mark(p, 5, st);
     k_radon_out<<<dim3(g.n_theta, nb), 256, g.n_rho * sizeof(float), st>>>(g, p->lp, sino);
-    mark(p, 6, st);
+    mark(p, 5, st);
     check_launch("radon launch");
-    p->launches += 6;
+    p->launches += 5;
     p->ffts += 2LL * g.M * nb;
 }
-const char* const kRadonStages[] = {"prefilter_rows", "prefilter_cols", "radon_theta_fwd", "rho_pass",
-                                    "theta_inv", "radon_out"};
+const char* const kRadonStages[] = {"prefilter_2d", "radon_theta_fwd", "rho_pass", "theta_inv", "radon_out"};
 
 void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
     mark(p, 0, st);
     k_prefilter_sino<<<dim3(cdiv(g.N, 256), g.n_theta, nb), 256, 0, st>>>(g, sino, p->qg);
     mark(p, 1, st);
-    k_bp_theta_fwd<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->qg, p->spec);
+    launch_bp_theta_fwd(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->qg, p->spec);
     mark(p, 2, st);
-    k_rho_pass<<<dim3(g.nts + 1, nb * g.M), p->t_rho, p->sm_rho, st>>>(g, p->d_rho, p->mult_B, p->spec);
+    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_B, p->spec);
     mark(p, 3, st);
-    k_theta_inv<<<dim3(cdiv(g.n_rho, 2), g.M, nb), p->t_coarse, p->sm_coarse, st>>>(g, p->d_coarse, p->spec, p->lp);
+    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->spec, p->lp);
     mark(p, 4, st);
     k_bp_out<<<dim3(cdiv(g.N, 128), g.N, nb), 128, 0, st>>>(g, p->lp, img);
     mark(p, 5, st);
@@ -357,6 +377,21 @@ void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, c
     p->launches += 5;
     p->ffts += 2LL * g.M * nb;
 }
+void transpose_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
+    const DevGeom& g = p->g;
+    k_radon_out_T<<<dim3(g.n_theta, nb), 256, g.n_rho * sizeof(float), st>>>(g, sino, p->lp);
+    launch_theta_fwd_T(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->lp, p->spec);
+    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_RT, p->spec);
+    ck(cudaMemsetAsync(p->qf, 0, sizeof(float) * size_t(nb) * g.pitch * g.pitch, st), "memset");
+    launch_theta_inv_fine_T(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->spec, p->qf);
+    k_prefilter_cols_T<<<dim3(cdiv(g.pitch, 256), g.N, nb), 256, 0, st>>>(g, p->band, p->band_h, p->qf, p->tmp);
+    const float scale = float(2.0 * p->geo.dtheta_p * p->geo.ds * double(g.N) * double(g.N));
+    k_prefilter_rows_T<<<dim3(cdiv(g.N, 256), g.N, nb), 256, 0, st>>>(g, p->band, p->band_h, p->tmp, img, scale);
+    check_launch("radon transpose launch");
+    p->launches += 6;
+    p->ffts += 2LL * g.M * nb;
+}
+
 const char* const kBackprojectStages[] = {"prefilter_sino", "bp_theta_fwd", "rho_pass", "theta_inv", "bp_out"};
 
 using ChunkFn = void (*)(lpr_gpu_plan*, const float*, float*, int, cudaStream_t);
@@ -488,12 +523,8 @@ int lpr_gpu_backproject_host(lpr_gpu_plan* p, const float* h_sino, float* h_img,
 
 int lpr_gpu_radon_transpose(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, void* stream) {
     return guard([&] {
-        (void)p;
-        (void)d_sino;
-        (void)d_img;
-        (void)batch;
-        (void)stream;
-        throw Error(LPR_ERR_CUDA, "radon_transpose: not built yet");
+        run_device(p, transpose_chunk, d_sino, d_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
+                   size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream);
     });
 }
 
@@ -504,7 +535,7 @@ int lpr_gpu_profile_stages(lpr_gpu_plan* p, int op, const float* d_in, float* d_
             throw std::invalid_argument("profile: bad arguments");
         if (op != 0 && op != 1) throw std::invalid_argument("profile: op must be 0 (R) or 1 (R#)");
         ck(cudaSetDevice(p->device), "cudaSetDevice");
-        const int ns = op == 0 ? 6 : 5;
+        const int ns = 5;
         std::vector<cudaEvent_t> ev(ns + 1);
         for (auto& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
         std::vector<double> acc(ns, 0.0);

@@ -1,0 +1,184 @@
+// Compile-time register FFTs for the plan lengths that dominate the hot path
+// (the 2048 / 8192 theta periods and the 7-smooth rho length 4374 of the
+// N=2048 bench plan, 16384 for N=4096). A transform runs in place in one
+// padded shared buffer: each pass stages all of a thread's butterflies in
+// registers between two barriers, with radices of 6..32 so a transform takes
+// 3-4 shared-memory round trips, and the index map pad(i) = i + i/16 keeps
+// the strided Stockham writes of the early passes (stride R float2) off
+// colliding banks.
+#pragma once
+
+#include "lpr_fft.cuh"
+
+namespace lpr {
+
+__constant__ float c_wr6[6] = {1.000000000e+00f, 5.000000000e-01f, -5.000000000e-01f, -1.000000000e+00f, -5.000000000e-01f, 5.000000000e-01f};
+__constant__ float c_wi6[6] = {0.000000000e+00f, -8.660254038e-01f, -8.660254038e-01f, -1.224646799e-16f, 8.660254038e-01f, 8.660254038e-01f};
+__constant__ float c_wr9[9] = {1.000000000e+00f, 7.660444431e-01f, 1.736481777e-01f, -5.000000000e-01f, -9.396926208e-01f, -9.396926208e-01f, -5.000000000e-01f, 1.736481777e-01f, 7.660444431e-01f};
+__constant__ float c_wi9[9] = {0.000000000e+00f, -6.427876097e-01f, -9.848077530e-01f, -8.660254038e-01f, -3.420201433e-01f, 3.420201433e-01f, 8.660254038e-01f, 9.848077530e-01f, 6.427876097e-01f};
+__constant__ float c_wr12[12] = {1.000000000e+00f, 8.660254038e-01f, 5.000000000e-01f, 6.123233996e-17f, -5.000000000e-01f, -8.660254038e-01f, -1.000000000e+00f, -8.660254038e-01f, -5.000000000e-01f, -1.836970199e-16f, 5.000000000e-01f, 8.660254038e-01f};
+__constant__ float c_wi12[12] = {0.000000000e+00f, -5.000000000e-01f, -8.660254038e-01f, -1.000000000e+00f, -8.660254038e-01f, -5.000000000e-01f, -1.224646799e-16f, 5.000000000e-01f, 8.660254038e-01f, 1.000000000e+00f, 8.660254038e-01f, 5.000000000e-01f};
+__constant__ float c_wr16[16] = {1.000000000e+00f, 9.238795325e-01f, 7.071067812e-01f, 3.826834324e-01f, 6.123233996e-17f, -3.826834324e-01f, -7.071067812e-01f, -9.238795325e-01f, -1.000000000e+00f, -9.238795325e-01f, -7.071067812e-01f, -3.826834324e-01f, -1.836970199e-16f, 3.826834324e-01f, 7.071067812e-01f, 9.238795325e-01f};
+__constant__ float c_wi16[16] = {0.000000000e+00f, -3.826834324e-01f, -7.071067812e-01f, -9.238795325e-01f, -1.000000000e+00f, -9.238795325e-01f, -7.071067812e-01f, -3.826834324e-01f, -1.224646799e-16f, 3.826834324e-01f, 7.071067812e-01f, 9.238795325e-01f, 1.000000000e+00f, 9.238795325e-01f, 7.071067812e-01f, 3.826834324e-01f};
+__constant__ float c_wr27[27] = {1.000000000e+00f, 9.730448706e-01f, 8.936326403e-01f, 7.660444431e-01f, 5.971585917e-01f, 3.960797660e-01f, 1.736481777e-01f, -5.814482891e-02f, -2.868032327e-01f, -5.000000000e-01f, -6.862416379e-01f, -8.354878114e-01f, -9.396926208e-01f, -9.932383577e-01f, -9.932383577e-01f, -9.396926208e-01f, -8.354878114e-01f, -6.862416379e-01f, -5.000000000e-01f, -2.868032327e-01f, -5.814482891e-02f, 1.736481777e-01f, 3.960797660e-01f, 5.971585917e-01f, 7.660444431e-01f, 8.936326403e-01f, 9.730448706e-01f};
+__constant__ float c_wi27[27] = {0.000000000e+00f, -2.306158707e-01f, -4.487991802e-01f, -6.427876097e-01f, -8.021231928e-01f, -9.182161069e-01f, -9.848077530e-01f, -9.983081583e-01f, -9.579895123e-01f, -8.660254038e-01f, -7.273736416e-01f, -5.495089781e-01f, -3.420201433e-01f, -1.160929141e-01f, 1.160929141e-01f, 3.420201433e-01f, 5.495089781e-01f, 7.273736416e-01f, 8.660254038e-01f, 9.579895123e-01f, 9.983081583e-01f, 9.848077530e-01f, 9.182161069e-01f, 8.021231928e-01f, 6.427876097e-01f, 4.487991802e-01f, 2.306158707e-01f};
+__constant__ float c_wr32[32] = {1.000000000e+00f, 9.807852804e-01f, 9.238795325e-01f, 8.314696123e-01f, 7.071067812e-01f, 5.555702330e-01f, 3.826834324e-01f, 1.950903220e-01f, 6.123233996e-17f, -1.950903220e-01f, -3.826834324e-01f, -5.555702330e-01f, -7.071067812e-01f, -8.314696123e-01f, -9.238795325e-01f, -9.807852804e-01f, -1.000000000e+00f, -9.807852804e-01f, -9.238795325e-01f, -8.314696123e-01f, -7.071067812e-01f, -5.555702330e-01f, -3.826834324e-01f, -1.950903220e-01f, -1.836970199e-16f, 1.950903220e-01f, 3.826834324e-01f, 5.555702330e-01f, 7.071067812e-01f, 8.314696123e-01f, 9.238795325e-01f, 9.807852804e-01f};
+__constant__ float c_wi32[32] = {0.000000000e+00f, -1.950903220e-01f, -3.826834324e-01f, -5.555702330e-01f, -7.071067812e-01f, -8.314696123e-01f, -9.238795325e-01f, -9.807852804e-01f, -1.000000000e+00f, -9.807852804e-01f, -9.238795325e-01f, -8.314696123e-01f, -7.071067812e-01f, -5.555702330e-01f, -3.826834324e-01f, -1.950903220e-01f, -1.224646799e-16f, 1.950903220e-01f, 3.826834324e-01f, 5.555702330e-01f, 7.071067812e-01f, 8.314696123e-01f, 9.238795325e-01f, 9.807852804e-01f, 1.000000000e+00f, 9.807852804e-01f, 9.238795325e-01f, 8.314696123e-01f, 7.071067812e-01f, 5.555702330e-01f, 3.826834324e-01f, 1.950903220e-01f};
+
+template <int R>
+__device__ __forceinline__ float2 wr(int j);
+#define LPR_WR(R)                                                                          \
+    template <>                                                                            \
+    __device__ __forceinline__ float2 wr<R>(int j) { return make_float2(c_wr##R[j], c_wi##R[j]); }
+LPR_WR(6)
+LPR_WR(9)
+LPR_WR(12)
+LPR_WR(16)
+LPR_WR(27)
+LPR_WR(32)
+#undef LPR_WR
+
+// Composite radix R = P * Q in registers, natural order in and out:
+// x[Q n1 + n2] -> P-point DFTs over n1, twiddle W_R^{n2 k1}, Q-point DFTs over n2
+// -> X[k1 + P k2].
+template <int P, int Q, bool INV>
+__device__ __forceinline__ void dft_pq(float2* v) {
+    constexpr int R = P * Q;
+    float2 y[Q][P];
+#pragma unroll
+    for (int n2 = 0; n2 < Q; ++n2) {
+        float2 t[P];
+#pragma unroll
+        for (int n1 = 0; n1 < P; ++n1) t[n1] = v[Q * n1 + n2];
+        Dft<P, INV>::run(t);
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) y[n2][k1] = t[k1];
+    }
+#pragma unroll
+    for (int n2 = 1; n2 < Q; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < P; ++k1) {
+            const float2 w = wr<R>((n2 * k1) % R);
+            y[n2][k1] = INV ? cmulc(y[n2][k1], w) : cmul(y[n2][k1], w);
+        }
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+        float2 t[Q];
+#pragma unroll
+        for (int n2 = 0; n2 < Q; ++n2) t[n2] = y[n2][k1];
+        Dft<Q, INV>::run(t);
+#pragma unroll
+        for (int k2 = 0; k2 < Q; ++k2) v[k1 + P * k2] = t[k2];
+    }
+}
+
+template <bool INV>
+struct Dft<6, INV> {
+    __device__ __forceinline__ static void run(float2* v) { dft_pq<2, 3, INV>(v); }
+};
+template <bool INV>
+struct Dft<9, INV> {
+    __device__ __forceinline__ static void run(float2* v) { dft_pq<3, 3, INV>(v); }
+};
+template <bool INV>
+struct Dft<12, INV> {
+    __device__ __forceinline__ static void run(float2* v) { dft_pq<4, 3, INV>(v); }
+};
+template <bool INV>
+struct Dft<16, INV> {
+    __device__ __forceinline__ static void run(float2* v) { dft_pq<4, 4, INV>(v); }
+};
+template <bool INV>
+struct Dft<27, INV> {
+    __device__ __forceinline__ static void run(float2* v) { dft_pq<3, 9, INV>(v); }
+};
+template <bool INV>
+struct Dft<32, INV> {
+    __device__ __forceinline__ static void run(float2* v) { dft_pq<4, 8, INV>(v); }
+};
+
+__host__ __device__ constexpr int ct_pad(int i) { return i + (i >> 4); }
+
+// One in-place pass of radix R at Stockham stride NS over a padded buffer.
+template <int N, int T, int R, int NS, bool INV>
+__device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw) {
+    constexpr int B = N / R;
+    constexpr int NB = (B + T - 1) / T;
+    constexpr int STRIDE = N / (NS * R);
+    const int tid = threadIdx.x;
+    float2 v[NB][R];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int b = tid + i * T;
+        if ((B % T == 0 && tid < T) || b < B) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[i][r] = x[ct_pad(b + r * B)];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int b = tid + i * T;
+        if ((B % T == 0 && tid < T) || b < B) {
+            const int k = b % NS;
+            if (NS > 1) {
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    const float2 w = __ldg(tw + k * r * STRIDE);
+                    v[i][r] = INV ? cmulc(v[i][r], w) : cmul(v[i][r], w);
+                }
+            }
+            Dft<R, INV>::run(v[i]);
+            const int base = (b - k) * R + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[ct_pad(base + r * NS)] = v[i][r];
+        }
+    }
+    __syncthreads();
+}
+
+template <int N, int T, bool INV, int NS, int R, int... Rest>
+__device__ __forceinline__ void ct_run(float2* x, const float2* tw) {
+    ct_pass<N, T, R, NS, INV>(x, tw);
+    if constexpr (sizeof...(Rest) > 0) ct_run<N, T, INV, NS * R, Rest...>(x, tw);
+}
+
+// FFT policies: both expose idx() (the buffer slot of element i), elems()
+// (shared float2 slots the kernel must allocate), threads() and run().
+template <int N, int T, int... R>
+struct CtFft {
+    static constexpr int kN = N;
+    static constexpr int kT = T;
+    __device__ __forceinline__ static int idx(int i) { return ct_pad(i); }
+    __host__ __device__ static int elems(const FftDesc&) { return ct_pad(N - 1) + 1; }
+    static int threads(const FftDesc&) { return T; }
+    template <bool INV>
+    __device__ __forceinline__ static float2* run(float2* x, float2*, const FftDesc& d) {
+        ct_run<N, T, INV, 1, R...>(x, d.tw);
+        return x;
+    }
+};
+
+struct GenericFft {
+    static constexpr int kN = 0;
+    __device__ __forceinline__ static int idx(int i) { return i; }
+    __host__ __device__ static int elems(const FftDesc& d) { return fft_smem_elems(d); }
+    static int threads(const FftDesc& d) {
+        const long len = d.nb ? d.nb : d.n;
+        long t = (len / 16 + 31) / 32 * 32;
+        return int(t < 64 ? 64 : (t > 512 ? 512 : t));
+    }
+    template <bool INV>
+    __device__ __forceinline__ static float2* run(float2* x, float2* scratch, const FftDesc& d) {
+        return block_fft<INV>(x, scratch, d, threadIdx.x, blockDim.x);
+    }
+};
+
+// The compile-time shapes, by length (host-side selection in lpr_capi.cu).
+using Fft2048 = CtFft<2048, 128, 16, 16, 8>;
+using Fft4096 = CtFft<4096, 256, 16, 16, 16>;
+using Fft4374 = CtFft<4374, 256, 6, 9, 9, 9>;
+using Fft8192 = CtFft<8192, 256, 32, 16, 16>;
+using Fft16384 = CtFft<16384, 512, 32, 32, 16>;
+
+}  // namespace lpr

@@ -2,7 +2,7 @@
 // Algorithm 1) and back-projection R# (Algorithm 2).
 //
 // Stage map (DESIGN.md §4 has the HBM layout and byte model of each):
-//   R : k_prefilter_rows -> k_prefilter_cols   (Alg.1 step 1, Qf)
+//   R : k_prefilter_2d     (Alg.1 step 1, Qf with a mirrored apron)
 //       k_radon_theta_fwd  gather T_m f e^rho on the fine grid Omega_lp,
 //                          zero-embed into the doubled theta period, real
 //                          theta FFT, keep |k_theta| < nts  (steps 3-6a)
@@ -11,6 +11,7 @@
 //       k_radon_out        S_m resampling to the sinogram, a_R^-1 (step 7)
 //   R#: k_prefilter_sino -> k_bp_theta_fwd -> k_rho_pass -> k_theta_inv
 //       -> k_bp_out (sector sum in ascending m, x2)
+#include "lpr_fft_ct.cuh"
 #include "lpr_kernels.cuh"
 
 namespace lpr {
@@ -49,65 +50,120 @@ __device__ __forceinline__ void bsw(float a, float w[4]) {
 // is a 33-tap separable FIR on the mirror-extended line: every output is
 // independent, so lines need no sequential scan and both passes coalesce.
 
-// rows: tmp[b][r][c'] for c' in [0, pitch), apron columns mirrored.
-__global__ void k_prefilter_rows(DevGeom g, const float* __restrict__ img, float* __restrict__ tmp) {
-    const int cp = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = blockIdx.y, b = blockIdx.z;
-    if (cp >= g.pitch) return;
-    const int N = g.N;
-    const float* src = img + (size_t(b) * N + r) * N;
-    const int c = mirror_idx(cp - kApron, N);
-    float acc = 0.f;
-#pragma unroll
-    for (int d = -kFirHalf; d <= kFirHalf; ++d) acc = fmaf(__ldg(g.fir + d + kFirHalf), __ldg(src + mirror_idx(c + d, N)), acc);
-    tmp[(size_t(b) * N + r) * g.pitch + cp] = acc;
-}
+// Because h is symmetric, the mirrored apron coefficient at x < 0 equals the
+// FIR over the virtually extended line, sum_d h_d f(mirror(x + d)), so one
+// 2-D tile kernel produces the apron-extended coefficient raster directly:
+// a (32 + 32)^2 input tile is staged in shared memory through the mirror
+// map, filtered along rows, then along columns (reference order: rows then
+// columns, bspline.cpp:120-129).
+constexpr int kPT = 32;                  // output tile edge
+constexpr int kPE = kPT + 2 * kFirHalf;  // staged input edge
 
-// cols: qf[b][r'][c'] over the apron-extended raster.
-__global__ void k_prefilter_cols(DevGeom g, const float* __restrict__ tmp, float* __restrict__ qf) {
-    const int cp = blockIdx.x * blockDim.x + threadIdx.x;
-    const int rp = blockIdx.y, b = blockIdx.z;
-    if (cp >= g.pitch) return;
-    const int N = g.N;
-    const float* src = tmp + size_t(b) * N * g.pitch + cp;
-    const int r = mirror_idx(rp - kApron, N);
-    float acc = 0.f;
+__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* __restrict__ img, float* __restrict__ qf) {
+    __shared__ float h[2 * kFirHalf + 1];
+    __shared__ float in[kPE][kPE + 1];
+    __shared__ float mid[kPE][kPT + 1];
+    const int tid = threadIdx.x;
+    const int N = g.N, pitch = g.pitch;
+    const int x0 = blockIdx.x * kPT, y0 = blockIdx.y * kPT, b = blockIdx.z;
+    if (tid < 2 * kFirHalf + 1) h[tid] = __ldg(g.fir + tid);
+    const float* src = img + size_t(b) * N * N;
+    const int vx0 = x0 - kApron - kFirHalf, vy0 = y0 - kApron - kFirHalf;
+    for (int i = tid / kPE; i < kPE; i += 256 / kPE) {
+        const float* row = src + size_t(mirror_idx(vy0 + i, N)) * N;
+        const int j = tid % kPE;
+        in[i][j] = __ldg(row + mirror_idx(vx0 + j, N));
+    }
+    __syncthreads();
+    for (int idx = tid; idx < kPE * kPT; idx += 256) {
+        const int i = idx / kPT, j = idx % kPT;
+        float acc = 0.f;
 #pragma unroll
-    for (int d = -kFirHalf; d <= kFirHalf; ++d)
-        acc = fmaf(__ldg(g.fir + d + kFirHalf), __ldg(src + size_t(mirror_idx(r + d, N)) * g.pitch), acc);
-    qf[(size_t(b) * g.pitch + rp) * g.pitch + cp] = acc;
+        for (int d = 0; d <= 2 * kFirHalf; ++d) acc = fmaf(h[d], in[i][j + d], acc);
+        mid[i][j] = acc;
+    }
+    __syncthreads();
+    float* dst = qf + size_t(b) * pitch * pitch;
+    for (int idx = tid; idx < kPT * kPT; idx += 256) {
+        const int i = idx / kPT, j = idx % kPT;
+        float acc = 0.f;
+#pragma unroll
+        for (int d = 0; d <= 2 * kFirHalf; ++d) acc = fmaf(h[d], mid[i + d][j], acc);
+        if (y0 + i < pitch && x0 + j < pitch) dst[size_t(y0 + i) * pitch + x0 + j] = acc;
+    }
 }
 
 // sinogram rows (R#, Alg. 2 step 1): prefilter along s only.
-__global__ void k_prefilter_sino(DevGeom g, const float* __restrict__ sino, float* __restrict__ qg) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i = blockIdx.y, b = blockIdx.z;
+__global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* __restrict__ sino, float* __restrict__ qg) {
+    __shared__ float h[2 * kFirHalf + 1];
+    __shared__ float in[256 + 2 * kFirHalf];
+    const int tid = threadIdx.x;
+    const int c0 = blockIdx.x * 256, i = blockIdx.y, b = blockIdx.z;
     const int N = g.N;
-    if (c >= N) return;
+    if (tid < 2 * kFirHalf + 1) h[tid] = __ldg(g.fir + tid);
     const float* src = sino + (size_t(b) * g.n_theta + i) * N;
+    for (int j = tid; j < 256 + 2 * kFirHalf; j += 256) in[j] = __ldg(src + mirror_idx(c0 - kFirHalf + j, N));
+    __syncthreads();
+    const int c = c0 + tid;
+    if (c >= N) return;
     float acc = 0.f;
 #pragma unroll
-    for (int d = -kFirHalf; d <= kFirHalf; ++d) acc = fmaf(__ldg(g.fir + d + kFirHalf), __ldg(src + mirror_idx(c + d, N)), acc);
+    for (int d = 0; d <= 2 * kFirHalf; ++d) acc = fmaf(h[d], in[tid + d], acc);
     qg[(size_t(b) * g.n_theta + i) * N + c] = acc;
 }
 
-// ------------------------------------------------------------- forward R
+// ------------------------------------------------------------- FFT-policy kernels
+// Every kernel with a transform is a template over the FFT policy F
+// (lpr_fft_ct.cuh): a compile-time register FFT for the hot lengths or the
+// generic runtime Stockham/Bluestein. F::idx maps element i to its shared slot.
+template <class F>
+__device__ __forceinline__ float2* fft_scratch(float2* sm, const FftDesc& d) {
+    return sm + (d.nb ? d.nb : d.n);
+}
+
 // Split the packed transform of z = a + i b into the half spectra of the
 // two real sequences and store them as columns l0, l0 + 1 of the sector's
 // (nts + 1) x n_rho spectral grid. The theta Nyquist row is zeroed
 // (|k_theta| < nts low-pass).
+template <class F>
 __device__ __forceinline__ void store_half_spectra(const float2* a, int L, int nts, int n_rho, int l0,
-                                                   float2* __restrict__ out, int gtid, int gsize) {
-    for (int k = gtid; k <= nts; k += gsize) {
+                                                   float2* __restrict__ out) {
+    for (int k = threadIdx.x; k <= nts; k += blockDim.x) {
         float2 A = make_float2(0.f, 0.f), B = A;
         if (k < nts) {
-            const float2 z = a[k], zm = a[k == 0 ? 0 : L - k];
+            const float2 z = a[F::idx(k)], zm = a[F::idx(k == 0 ? 0 : L - k)];
             A = make_float2(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y));
             B = make_float2(0.5f * (z.y + zm.y), -0.5f * (z.x - zm.x));
         }
         float2* row = out + size_t(k) * n_rho;
-        row[l0] = A;
-        if (l0 + 1 < n_rho) row[l0 + 1] = B;
+        if (l0 + 1 < n_rho && ((size_t(k) * n_rho + l0) & 1) == 0) {
+            *reinterpret_cast<float4*>(row + l0) = make_float4(A.x, A.y, B.x, B.y);
+        } else {
+            row[l0] = A;
+            if (l0 + 1 < n_rho) row[l0 + 1] = B;
+        }
+    }
+}
+
+// Load the half spectra of columns l0, l0 + 1 (k in [0, kmax)) and rebuild
+// the packed Hermitian transform of length L: Z(k) = A + iB, Z(L-k) = conj(A) + i conj(B).
+template <class F>
+__device__ __forceinline__ void load_packed_hermitian(float2* sm, const float2* __restrict__ in, int kmax, int L,
+                                                      int n, int l0) {
+    const bool two = l0 + 1 < n;
+    for (int k = threadIdx.x; k < kmax; k += blockDim.x) {
+        const float2* p = in + size_t(k) * n + l0;
+        float2 A, B;
+        if (two && ((size_t(k) * n + l0) & 1) == 0) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+            A = make_float2(v.x, v.y);
+            B = make_float2(v.z, v.w);
+        } else {
+            A = p[0];
+            B = two ? p[1] : make_float2(0.f, 0.f);
+        }
+        sm[F::idx(k)] = make_float2(A.x - B.y, A.y + B.x);
+        if (k > 0) sm[F::idx(L - k)] = make_float2(A.x + B.y, B.x - A.y);
     }
 }
 
@@ -134,13 +190,19 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const float* __r
     return er * acc;
 }
 
-__global__ void __launch_bounds__(512) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float* __restrict__ qf, float2* __restrict__ spec) {
+// Alg. 1 steps 3-6a: gather T_m f e^rho on the fine grid of two rho columns,
+// zero-embed into the doubled fine period Lf, real theta FFT, keep |k| < nts.
+template <class F>
+__global__ void __launch_bounds__(512) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                                         const float* __restrict__ qf, float2* __restrict__ spec) {
     extern __shared__ float2 sm[];
     const int tid = threadIdx.x, T = blockDim.x;
     const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
     const int Lf = g.Lf, nf = g.nf;
-    for (int i = tid; i < Lf; i += T) sm[i] = make_float2(0.f, 0.f);
-    __syncthreads();
+    for (int i = tid; i < Lf / 4; i += T) {  // the zero half [nf/2, Lf - nf/2)
+        sm[F::idx(nf / 2 + i)] = make_float2(0.f, 0.f);
+        sm[F::idx(nf / 2 + Lf / 4 + i)] = make_float2(0.f, 0.f);
+    }
     const float* q = qf + size_t(b) * g.pitch * g.pitch;
     const float cm = g.cosm[m], smm = g.sinm[m];
     const float er0 = __ldg(g.erho + l0);
@@ -151,57 +213,59 @@ __global__ void __launch_bounds__(512) k_radon_theta_fwd(const __grid_constant__
         const float h0 = gather_image(g, q, cm, smm, er0, ct, st);
         const float h1 = two ? gather_image(g, q, cm, smm, er1, ct, st) : 0.f;
         const int qq = i - nf / 2;
-        sm[qq < 0 ? qq + Lf : qq] = make_float2(h0, h1);
+        sm[F::idx(qq < 0 ? qq + Lf : qq)] = make_float2(h0, h1);
     }
     __syncthreads();
-    const float2* res = block_fft<false>(sm, sm + (fd.nb ? fd.nb : fd.n), fd, tid, T);
+    const float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd);
     float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
-    store_half_spectra(res, Lf, g.nts, g.n_rho, l0, out, tid, T);
+    store_half_spectra<F>(res, Lf, g.nts, g.n_rho, l0, out);
 }
 
 // rho pass: for every (item, k_theta) row, FFT along rho, multiply by the
 // kernel spectrum row, inverse FFT. One block per row; the multiplier row is
 // shared by all items of the batch (grid.y).
-__global__ void __launch_bounds__(512) k_rho_pass(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float2* __restrict__ mult, float2* __restrict__ spec) {
+template <class F>
+__global__ void __launch_bounds__(512) k_rho_pass(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                                  const float2* __restrict__ mult, float2* __restrict__ spec) {
     extern __shared__ float2 sm[];
     const int tid = threadIdx.x, T = blockDim.x;
     const int k = blockIdx.x, item = blockIdx.y;
     const int n = g.n_rho;
     float2* row = spec + (size_t(item) * (g.nts + 1) + k) * n;
-    const int len = fd.nb ? fd.nb : fd.n;
-    for (int j = tid; j < n; j += T) sm[j] = row[j];
+    for (int j = tid; j < n; j += T) sm[F::idx(j)] = row[j];
     __syncthreads();
-    float2* a = block_fft<false>(sm, sm + len, fd, tid, T);
+    float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd);
     const float2* mrow = mult + size_t(k) * n;
-    for (int j = tid; j < n; j += T) a[j] = cmul(a[j], __ldg(mrow + j));
+    for (int j = tid; j < n; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], __ldg(mrow + j));
     __syncthreads();
-    a = block_fft<true>(a, a == sm ? sm + len : sm, fd, tid, T);
-    for (int j = tid; j < n; j += T) row[j] = a[j];
+    a = F::template run<true>(a, a == sm ? fft_scratch<F>(sm, fd) : sm, fd);
+    for (int j = tid; j < n; j += T) row[j] = a[F::idx(j)];
 }
 
 // Hermitian theta inverse: two real columns per complex transform of length
 // 2 nts; rows [j0, j0 + win) of the periodic result are kept.
-__global__ void __launch_bounds__(512) k_theta_inv(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float2* __restrict__ spec, float* __restrict__ lp) {
+template <class F>
+__global__ void __launch_bounds__(512) k_theta_inv(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                                   const float2* __restrict__ spec, float* __restrict__ lp) {
     extern __shared__ float2 sm[];
     const int tid = threadIdx.x, T = blockDim.x;
     const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
     const int nts = g.nts, L2 = g.L2, n = g.n_rho;
     const bool two = l0 + 1 < n;
     const size_t item = size_t(b) * g.M + m;
-    const float2* in = spec + item * size_t(nts + 1) * n;
-    for (int k = tid; k <= nts; k += T) {
-        const float2 A = in[size_t(k) * n + l0];
-        const float2 B = two ? in[size_t(k) * n + l0 + 1] : make_float2(0.f, 0.f);
-        sm[k] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
-        if (k > 0 && k < nts) sm[L2 - k] = make_float2(A.x + B.y, B.x - A.y);  // conj(A) + i conj(B)
-    }
+    if (tid == 0) sm[F::idx(nts)] = make_float2(0.f, 0.f);  // Nyquist bin (zeroed band edge)
+    load_packed_hermitian<F>(sm, spec + item * size_t(nts + 1) * n, nts, L2, n, l0);
     __syncthreads();
-    const float2* res = block_fft<true>(sm, sm + (fd.nb ? fd.nb : fd.n), fd, tid, T);
+    const float2* res = F::template run<true>(sm, fft_scratch<F>(sm, fd), fd);
     float* out = lp + item * size_t(g.win) * n;
     for (int r = tid; r < g.win; r += T) {
-        const float2 z = res[wrapi(g.j0 + r, L2)];
-        out[size_t(r) * n + l0] = z.x;
-        if (two) out[size_t(r) * n + l0 + 1] = z.y;
+        const float2 z = res[F::idx(wrapi(g.j0 + r, L2))];
+        if (two && ((size_t(r) * n + l0) & 1) == 0) {
+            *reinterpret_cast<float2*>(out + size_t(r) * n + l0) = z;
+        } else {
+            out[size_t(r) * n + l0] = z.x;
+            if (two) out[size_t(r) * n + l0 + 1] = z.y;
+        }
     }
 }
 
@@ -261,13 +325,14 @@ __device__ __forceinline__ float gather_sino(const float* __restrict__ row, int 
 // g(S_m^{-1}) on Omega_p (Alg. 2 step 3): theta' rows are polar rows, so each
 // sample is a 1-D spline along s (zero outside the detector), then the real
 // theta FFT of the zero-embedded doubled period.
-__global__ void __launch_bounds__(512) k_bp_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd, const float* __restrict__ qg, float2* __restrict__ spec) {
+template <class F>
+__global__ void __launch_bounds__(512) k_bp_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                                      const float* __restrict__ qg, float2* __restrict__ spec) {
     extern __shared__ float2 sm[];
     const int tid = threadIdx.x, T = blockDim.x;
     const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
     const int nts = g.nts, L2 = g.L2, N = g.N;
-    for (int i = tid; i < L2; i += T) sm[i] = make_float2(0.f, 0.f);
-    __syncthreads();
+    for (int i = tid; i < nts; i += T) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
     const bool two = l0 + 1 < g.n_rho;
     const float er0 = __ldg(g.erho + l0);
     const float er1 = two ? __ldg(g.erho + l0 + 1) : 0.f;
@@ -285,12 +350,81 @@ __global__ void __launch_bounds__(512) k_bp_theta_fwd(const __grid_constant__ De
         const float v0 = gather_sino(row, N, t0);
         float v1 = 0.f;
         if (two) v1 = gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN));
-        sm[j < 0 ? j + L2 : j] = make_float2(v0, v1);
+        sm[F::idx(j < 0 ? j + L2 : j)] = make_float2(v0, v1);
     }
     __syncthreads();
-    const float2* res = block_fft<false>(sm, sm + (fd.nb ? fd.nb : fd.n), fd, tid, T);
+    const float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd);
     float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * g.n_rho;
-    store_half_spectra(res, L2, nts, g.n_rho, l0, out, tid, T);
+    store_half_spectra<F>(res, L2, nts, g.n_rho, l0, out);
+}
+
+// R^T stage 2: real theta FFT of the lattice rows [-nts/2, nts/2) held in
+// the window buffer (the transpose of the forward theta inverse + crop).
+template <class F>
+__global__ void __launch_bounds__(512) k_theta_fwd_T(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                                     const float* __restrict__ lp, float2* __restrict__ spec) {
+    extern __shared__ float2 sm[];
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
+    const int nts = g.nts, L2 = g.L2, n = g.n_rho;
+    const bool two = l0 + 1 < n;
+    for (int i = tid; i < nts; i += T) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
+    const float* in = lp + (size_t(b) * g.M + m) * size_t(g.win) * n;
+    for (int jj = tid; jj < nts; jj += T) {
+        const int j = jj - nts / 2;
+        const float* row = in + size_t(j - g.j0) * n;
+        sm[F::idx(j < 0 ? j + L2 : j)] = make_float2(row[l0], two ? row[l0 + 1] : 0.f);
+    }
+    __syncthreads();
+    const float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd);
+    float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * n;
+    store_half_spectra<F>(res, L2, nts, n, l0, out);
+}
+
+// R^T stage 4: Hermitian inverse over the doubled fine period (zero beyond
+// |k| < nts) and the transposed fine-grid gather G_m^T, scattering the spline
+// taps into the apron-extended coefficient image.
+template <class F>
+__global__ void __launch_bounds__(512) k_theta_inv_fine_T(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                                          const float2* __restrict__ spec, float* __restrict__ qbar) {
+    extern __shared__ float2 sm[];
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
+    const int nts = g.nts, Lf = g.Lf, n = g.n_rho, nf = g.nf;
+    const bool two = l0 + 1 < n;
+    const size_t item = size_t(b) * g.M + m;
+    for (int k = nts + tid; k <= Lf - nts; k += T) sm[F::idx(k)] = make_float2(0.f, 0.f);
+    load_packed_hermitian<F>(sm, spec + item * size_t(nts + 1) * n, nts, Lf, n, l0);
+    __syncthreads();
+    const float2* res = F::template run<true>(sm, fft_scratch<F>(sm, fd), fd);
+    float* q = qbar + size_t(b) * g.pitch * g.pitch;
+    const float cm = g.cosm[m], smm = g.sinm[m];
+    const float half = 0.5f * g.N;
+    for (int i = tid; i < nf; i += T) {
+        const int qq = i - nf / 2;
+        const float2 z = res[F::idx(qq < 0 ? qq + Lf : qq)];
+        const float ct = __ldg(g.fine_cos + i), st = __ldg(g.fine_sin + i);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            if (c == 1 && !two) break;
+            const float er = __ldg(g.erho + l0 + c);
+            const float dx = fmaf(er, ct, -g.one_m_aR), dy = er * st;
+            if (fmaf(dx, dx, dy * dy) > g.aR2) continue;
+            const float ux = dx * g.inv_aR, uy = dy * g.inv_aR;
+            const float xp = fmaf(cm, ux, -smm * uy), yp = fmaf(smm, ux, cm * uy);
+            const float tc = fmaf(xp, half, half), tr = fmaf(yp, half, half);
+            const float kc = floorf(tc), kr = floorf(tr);
+            float wc[4], wr[4];
+            bsw(tc - kc, wc);
+            bsw(tr - kr, wr);
+            const float v = er * (c == 0 ? z.x : z.y);
+            float* p = q + (int(kr) - 1 + kApron) * g.pitch + (int(kc) - 1 + kApron);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) atomicAdd(p + a * g.pitch + e, v * wr[a] * wc[e]);
+        }
+    }
 }
 
 // T_m^{-1} Omega_p -> X resampling and the sector sum (Alg. 2 steps 5-7).
@@ -338,6 +472,97 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         acc += sacc;
     }
     *out = 2.f * acc;
+}
+
+// ------------------------------------------------------------- host launchers
+FftLaunch fft_launch_config(const FftDesc& d) {
+    FftLaunch L{kFftGeneric, GenericFft::threads(d), size_t(GenericFft::elems(d)) * sizeof(float2)};
+    if (d.nb != 0) return L;
+#define LPR_PICK(F, ID)                                                          \
+    if (d.n == F::kN) return FftLaunch{ID, F::kT, size_t(F::elems(d)) * sizeof(float2)};
+    LPR_PICK(Fft2048, kFft2048)
+    LPR_PICK(Fft4096, kFft4096)
+    LPR_PICK(Fft4374, kFft4374)
+    LPR_PICK(Fft8192, kFft8192)
+    LPR_PICK(Fft16384, kFft16384)
+#undef LPR_PICK
+    return L;
+}
+
+#define LPR_FFT_SWITCH(var, CALL)      \
+    switch (var) {                     \
+        case kFft2048: CALL(Fft2048); break;   \
+        case kFft4096: CALL(Fft4096); break;   \
+        case kFft4374: CALL(Fft4374); break;   \
+        case kFft8192: CALL(Fft8192); break;   \
+        case kFft16384: CALL(Fft16384); break; \
+        default: CALL(GenericFft); break;      \
+    }
+
+static cudaError_t smem_attr(const void* fn, size_t bytes) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse) {
+    cudaError_t e = cudaSuccess;
+#define SET(K, L)                                                              \
+    do {                                                                       \
+        cudaError_t r = smem_attr((const void*)K, L.smem);                     \
+        if (r != cudaSuccess) e = r;                                           \
+    } while (0)
+#define FINE(F) SET(k_radon_theta_fwd<F>, fine); SET(k_theta_inv_fine_T<F>, fine)
+#define RHO(F) SET(k_rho_pass<F>, rho)
+#define COARSE(F) SET(k_theta_inv<F>, coarse); SET(k_bp_theta_fwd<F>, coarse); SET(k_theta_fwd_T<F>, coarse)
+    LPR_FFT_SWITCH(fine.variant, FINE)
+    LPR_FFT_SWITCH(rho.variant, RHO)
+    LPR_FFT_SWITCH(coarse.variant, COARSE)
+#undef FINE
+#undef RHO
+#undef COARSE
+#undef SET
+    return e;
+}
+
+void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                            const float* qf, float2* spec) {
+#define CALL(F) k_radon_theta_fwd<F><<<grid, L.threads, L.smem, st>>>(g, fd, qf, spec)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+}
+
+void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                     const float2* mult, float2* spec) {
+#define CALL(F) k_rho_pass<F><<<grid, L.threads, L.smem, st>>>(g, fd, mult, spec)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+}
+
+void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                      const float2* spec, float* lp) {
+#define CALL(F) k_theta_inv<F><<<grid, L.threads, L.smem, st>>>(g, fd, spec, lp)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+}
+
+void launch_bp_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                         const float* qg, float2* spec) {
+#define CALL(F) k_bp_theta_fwd<F><<<grid, L.threads, L.smem, st>>>(g, fd, qg, spec)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+}
+
+void launch_theta_fwd_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                        const float* lp, float2* spec) {
+#define CALL(F) k_theta_fwd_T<F><<<grid, L.threads, L.smem, st>>>(g, fd, lp, spec)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+}
+
+void launch_theta_inv_fine_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                             const float2* spec, float* qbar) {
+#define CALL(F) k_theta_inv_fine_T<F><<<grid, L.threads, L.smem, st>>>(g, fd, spec, qbar)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
 }
 
 }  // namespace lpr

@@ -31,4 +31,29 @@ struct DevGeom {
     const float* fir;         // 2 kFirHalf + 1 prefilter taps
 };
 
+// FFT kernel variants: a compile-time register FFT for the hot lengths
+// (lpr_fft_ct.cuh) or the generic runtime Stockham / Bluestein.
+enum FftVariant : int { kFftGeneric = 0, kFft2048, kFft4096, kFft4374, kFft8192, kFft16384 };
+struct FftLaunch {
+    int variant;
+    int threads;
+    size_t smem;
+};
+
+// host-side launchers (lpr_kernels.cu)
+FftLaunch fft_launch_config(const FftDesc& d);
+cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse);
+void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                            const float* qf, float2* spec);
+void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                     const float2* mult, float2* spec);
+void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                      const float2* spec, float* lp);
+void launch_bp_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                         const float* qg, float2* spec);
+void launch_theta_fwd_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                        const float* lp, float2* spec);
+void launch_theta_inv_fine_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                             const float2* spec, float* qbar);
+
 }  // namespace lpr

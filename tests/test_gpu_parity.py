@@ -28,7 +28,7 @@ def _inputs(lpo, N, n):
 
 
 @pytest.mark.parametrize("N,smooth", [(64, False), (128, False), (256, False), (256, True), (512, False),
-                                      (512, True)])
+                                      (512, True), (1024, True)])
 def test_radon_and_backprojection_parity(lp, lpo, cuda, N, smooth):
     import torch
 
@@ -145,3 +145,32 @@ def test_sinogram_of_disc_is_rotation_invariant(lp, lpo, cuda):
     want = 2 * np.sqrt(np.clip(0.04 - x ** 2, 0, None))
     assert lpo.rel_l2(s.mean(axis=0), want) <= 5e-3
     assert np.abs(s - s.mean(axis=0)).max() <= 1e-2 * want.max()
+
+
+@pytest.mark.parametrize("N", [64, 256])
+def test_exact_transpose_adjoint_identity(lp, lpo, cuda, N):
+    """<R f, g>_Sigma = <f, R^T g>_X to 1e-5 (north star), fp64 inner products
+    of fp32 GPU outputs; and R^T itself against the oracle's transpose."""
+    import torch
+
+    g, p, z, zb, plan = _setup(lp, lpo, N)
+    rng = np.random.default_rng(7)
+    for trial in range(3):
+        f = lpo.smooth_disc_image(N, 0.9, 100 + trial) if trial else rng.uniform(-1, 1, (N, N))
+        rf = lp.fast_radon(torch.tensor(f, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+        s = rf.astype(np.float64) + 0.3 * rng.uniform(-1, 1, rf.shape) * np.abs(rf).max()
+        rts = lp.radon_transpose(torch.tensor(s, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+        f32 = f.astype(np.float32).astype(np.float64)
+        s32 = s.astype(np.float32).astype(np.float64)
+        a = lp.inner_sinogram(g, rf, s32)
+        b = lp.inner_image(g, f32, rts)
+        assert abs(a - b) <= 1e-5 * abs(a), (trial, a, b)
+        gap = abs(a - b) / np.sqrt(lp.inner_image(g, f32, f32) * lp.inner_sinogram(g, s32, s32))
+        assert gap <= 1e-5
+    want = lpo.radon_transpose(p, z, s32)
+    assert lpo.rel_l2(rts, want) <= TOL
+
+
+def test_adjoint_gap_exact_gpu(lp, lpo, cuda):
+    g, p, z, zb, plan = _setup(lp, lpo, 64)
+    assert lp.adjoint_gap(plan, trials=5, exact=True) <= 1e-5
