@@ -1,0 +1,49 @@
+// lp_ops.hpp — the fast log-polar operators of the reference's (specified,
+// unimplemented) lp_ops module, as a drop-in for
+// proj/src/lp_ops.cpp:1-2 (empty namespace upstream). The declarations follow
+// SPEC.md:267-308 and the reference's value-type conventions
+// (proj/include/lpradon/types.hpp:10-74): Image / Sinogram returned by value,
+// preconditions via require() -> std::invalid_argument, device failures ->
+// std::runtime_error.
+//
+// The implementation (paper_1506_00014_b200/csrc/dropin/lp_ops.cpp) is a thin
+// C++ layer over the C ABI in lpradon_gpu.h: fp64 rasters are staged to fp32,
+// the plan owns the uploaded spectra (zeta_spectrum / zeta_bp_spectrum from
+// the reference's kernel.cpp) and every operator runs on the B200. Include
+// this from a tree that provides the reference headers (lpradon/types.hpp,
+// geometry.hpp, kernel.hpp).
+#pragma once
+
+#include <memory>
+
+#include "lpradon/geometry.hpp"
+#include "lpradon/kernel.hpp"
+#include "lpradon/types.hpp"
+
+struct lpr_gpu_plan;
+
+namespace lpr {
+
+/// geometry + both kernel spectra + the device plan.
+/// Immutable after construction and shareable; one plan per device.
+struct RadonPlan {
+    GeometryPlan geom;
+    KernelSpectrum zeta, zeta_bp;
+    int device = 0;
+    int max_batch = 1;
+    std::shared_ptr<lpr_gpu_plan> gpu;
+};
+
+RadonPlan make_radon_plan(const GeometryPlan& geom, KernelMethod method = KernelMethod::quadrature,
+                          int device = 0, int max_batch = 1);
+
+/// Algorithm 1.
+Sinogram fast_radon(const Image& image, const RadonPlan& plan);
+/// Algorithm 2.
+Image fast_backprojection(const Sinogram& sino, const RadonPlan& plan);
+/// Exact discrete adjoint of fast_radon under the adjoint_gap inner products.
+Image radon_transpose(const Sinogram& sino, const RadonPlan& plan);
+/// max over `trials` random pairs of |<Rf,g> - <f,R#g>| / (|f||g|).
+double adjoint_gap(const RadonPlan& plan, int trials);
+
+}  // namespace lpr

@@ -84,6 +84,7 @@ int lpr_gpu_radon_transpose(lpr_gpu_plan* plan, const float* d_sino, float* d_im
  * stream synchronisation inside the call (the end-to-end path). */
 int lpr_gpu_radon_host(lpr_gpu_plan* plan, const float* h_img, float* h_sino, int batch);
 int lpr_gpu_backproject_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int batch);
+int lpr_gpu_radon_transpose_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int batch);
 
 /* Instrumentation: run one chunk of op (0 = R, 1 = R#) on device buffers
  * `reps` times on the plan's stream with CUDA events between the launches;

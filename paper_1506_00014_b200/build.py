@@ -87,5 +87,28 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+REF_INCLUDE = "/root/reference/proj/include"
+REF_LIB = os.path.join(ROOT, "oracle", "_ref", "liblpr_ref.so")
+DROPIN = os.path.join(PKG, "_dropin", "dropin_smoke")
+
+
+def build_dropin() -> str | None:
+    """The C++ drop-in layer (include/lpradon/lp_ops.hpp, csrc/dropin/lp_ops.cpp)
+    compiled against the reference's own headers, with a smoke driver linked to
+    the reference's compiled blocks (oracle/_ref). Only where /root/reference
+    exists; the binary then travels to the GPU box with the tree."""
+    if not (os.path.isdir(REF_INCLUDE) and os.path.exists(REF_LIB) and os.path.exists(LIB)):
+        return None
+    os.makedirs(os.path.dirname(DROPIN), exist_ok=True)
+    srcs = [os.path.join(CSRC, "dropin", "lp_ops.cpp"), os.path.join(ROOT, "tests", "dropin", "dropin_smoke.cpp")]
+    if not _stale(DROPIN, srcs + [LIB, REF_LIB, os.path.join(ROOT, "include", "lpradon", "lp_ops.hpp")]):
+        return DROPIN
+    _run([_host_cxx(), "-O2", "-std=c++20", "-I" + os.path.join(ROOT, "include"), "-I" + REF_INCLUDE, *srcs,
+          "-o", DROPIN, LIB, REF_LIB, "-Wl,-rpath,$ORIGIN/..:$ORIGIN/../../oracle/_ref",
+          "/usr/lib/x86_64-linux-gnu/libmpfr.so.6", "/usr/lib/x86_64-linux-gnu/libgmp.so.10", "-fopenmp"],
+         os.path.join(BUILD, "dropin.log"))
+    return DROPIN
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))

@@ -181,7 +181,8 @@ struct lpr_gpu_plan {
             d.bhat = upload(bh);
         }
         launch = fft_launch_config(d);
-        if (launch.smem > 227 * 1024) throw std::invalid_argument("fft: transform does not fit in shared memory");
+        if (launch.smem * launch.per_block > 227 * 1024)
+            throw std::invalid_argument("fft: transform does not fit in shared memory");
     }
 
     ~lpr_gpu_plan() {
@@ -517,6 +518,13 @@ int lpr_gpu_radon_host(lpr_gpu_plan* p, const float* h_img, float* h_sino, int b
 int lpr_gpu_backproject_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batch) {
     return guard([&] {
         run_host(p, backproject_chunk, h_sino, h_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
+                 size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0));
+    });
+}
+
+int lpr_gpu_radon_transpose_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batch) {
+    return guard([&] {
+        run_host(p, transpose_chunk, h_sino, h_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
                  size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0));
     });
 }

@@ -101,16 +101,15 @@ __host__ __device__ constexpr int ct_pad(int i) { return i + (i >> 4); }
 
 // One in-place pass of radix R at Stockham stride NS over a padded buffer.
 template <int N, int T, int R, int NS, bool INV>
-__device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw) {
+__device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw, int tid) {
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
     constexpr int STRIDE = N / (NS * R);
-    const int tid = threadIdx.x;
     float2 v[NB][R];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int b = tid + i * T;
-        if ((B % T == 0 && tid < T) || b < B) {
+        if (b < B) {
 #pragma unroll
             for (int r = 0; r < R; ++r) v[i][r] = x[ct_pad(b + r * B)];
         }
@@ -119,7 +118,7 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int b = tid + i * T;
-        if ((B % T == 0 && tid < T) || b < B) {
+        if (b < B) {
             const int k = b % NS;
             if (NS > 1) {
 #pragma unroll
@@ -138,29 +137,37 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
 }
 
 template <int N, int T, bool INV, int NS, int R, int... Rest>
-__device__ __forceinline__ void ct_run(float2* x, const float2* tw) {
-    ct_pass<N, T, R, NS, INV>(x, tw);
-    if constexpr (sizeof...(Rest) > 0) ct_run<N, T, INV, NS * R, Rest...>(x, tw);
+__device__ __forceinline__ void ct_run(float2* x, const float2* tw, int tid) {
+    ct_pass<N, T, R, NS, INV>(x, tw, tid);
+    if constexpr (sizeof...(Rest) > 0) ct_run<N, T, INV, NS * R, Rest...>(x, tw, tid);
 }
 
-// FFT policies: both expose idx() (the buffer slot of element i), elems()
-// (shared float2 slots the kernel must allocate), threads() and run().
-template <int N, int T, int... R>
+// FFT policies: idx() (the buffer slot of element i), elems() (shared
+// float2 slots one transform needs), kT threads per transform and kP
+// transforms per block (the theta kernels give each transform two real
+// columns, so kP pairs make 4 kP contiguous columns per global row access),
+// kMinBlocks for __launch_bounds__, and run() on the calling thread group
+// (gtid in [0, kT); every thread of the block must call it).
+template <int N, int T, int P, int MINB, int... R>
 struct CtFft {
     static constexpr int kN = N;
     static constexpr int kT = T;
+    static constexpr int kP = P;
+    static constexpr int kMinBlocks = MINB;
     __device__ __forceinline__ static int idx(int i) { return ct_pad(i); }
     __host__ __device__ static int elems(const FftDesc&) { return ct_pad(N - 1) + 1; }
-    static int threads(const FftDesc&) { return T; }
     template <bool INV>
-    __device__ __forceinline__ static float2* run(float2* x, float2*, const FftDesc& d) {
-        ct_run<N, T, INV, 1, R...>(x, d.tw);
+    __device__ __forceinline__ static float2* run(float2* x, float2*, const FftDesc& d, int gtid) {
+        ct_run<N, T, INV, 1, R...>(x, d.tw, gtid);
         return x;
     }
 };
 
 struct GenericFft {
     static constexpr int kN = 0;
+    static constexpr int kT = 0;  // runtime: threads(d)
+    static constexpr int kP = 1;
+    static constexpr int kMinBlocks = 1;
     __device__ __forceinline__ static int idx(int i) { return i; }
     __host__ __device__ static int elems(const FftDesc& d) { return fft_smem_elems(d); }
     static int threads(const FftDesc& d) {
@@ -169,16 +176,17 @@ struct GenericFft {
         return int(t < 64 ? 64 : (t > 512 ? 512 : t));
     }
     template <bool INV>
-    __device__ __forceinline__ static float2* run(float2* x, float2* scratch, const FftDesc& d) {
-        return block_fft<INV>(x, scratch, d, threadIdx.x, blockDim.x);
+    __device__ __forceinline__ static float2* run(float2* x, float2* scratch, const FftDesc& d, int gtid) {
+        return block_fft<INV>(x, scratch, d, gtid, blockDim.x);
     }
 };
 
 // The compile-time shapes, by length (host-side selection in lpr_capi.cu).
-using Fft2048 = CtFft<2048, 128, 16, 16, 8>;
-using Fft4096 = CtFft<4096, 256, 16, 16, 16>;
-using Fft4374 = CtFft<4374, 256, 6, 9, 9, 9>;
-using Fft8192 = CtFft<8192, 256, 32, 16, 16>;
-using Fft16384 = CtFft<16384, 512, 32, 32, 16>;
+//                   N      T   P  minB  radices
+using Fft2048 = CtFft<2048, 128, 4, 2, 16, 16, 8>;
+using Fft4096 = CtFft<4096, 256, 2, 1, 16, 16, 16>;
+using Fft4374 = CtFft<4374, 256, 1, 3, 6, 9, 9, 9>;
+using Fft8192 = CtFft<8192, 256, 1, 2, 32, 16, 16>;
+using Fft16384 = CtFft<16384, 512, 1, 1, 32, 32, 16>;
 
 }  // namespace lpr

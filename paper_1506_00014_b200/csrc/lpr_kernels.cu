@@ -11,6 +11,8 @@
 //       k_radon_out        S_m resampling to the sinogram, a_R^-1 (step 7)
 //   R#: k_prefilter_sino -> k_bp_theta_fwd -> k_rho_pass -> k_theta_inv
 //       -> k_bp_out (sector sum in ascending m, x2)
+#include <cstdint>
+
 #include "lpr_fft_ct.cuh"
 #include "lpr_kernels.cuh"
 
@@ -115,55 +117,85 @@ __global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* 
 // ------------------------------------------------------------- FFT-policy kernels
 // Every kernel with a transform is a template over the FFT policy F
 // (lpr_fft_ct.cuh): a compile-time register FFT for the hot lengths or the
-// generic runtime Stockham/Bluestein. F::idx maps element i to its shared slot.
+// generic runtime Stockham/Bluestein. F::idx maps element i to its shared
+// slot. Theta kernels run F::kP transforms per block, one per thread group,
+// each on a pair of real columns packed as re/im, so a block touches 4 kP
+// contiguous complex columns per spectral row.
+template <class F>
+struct Group {
+    int g, tid, size;
+    __device__ __forceinline__ Group() {
+        if constexpr (F::kT > 0) {
+            size = F::kT;
+            g = threadIdx.x / F::kT;
+            tid = threadIdx.x % F::kT;
+        } else {
+            size = blockDim.x;
+            g = 0;
+            tid = threadIdx.x;
+        }
+    }
+};
+
+#define LPR_LB(F) __launch_bounds__((F::kT > 0 ? F::kT * F::kP : 512), F::kMinBlocks)
+
 template <class F>
 __device__ __forceinline__ float2* fft_scratch(float2* sm, const FftDesc& d) {
     return sm + (d.nb ? d.nb : d.n);
 }
 
-// Split the packed transform of z = a + i b into the half spectra of the
-// two real sequences and store them as columns l0, l0 + 1 of the sector's
-// (nts + 1) x n_rho spectral grid. The theta Nyquist row is zeroed
-// (|k_theta| < nts low-pass).
+// Pair the block's columns: pair p of the block covers columns l0 + 2p, l0 + 2p + 1.
+__device__ __forceinline__ bool col_ok(int l, int n) { return l < n; }
+
+// Split the packed transforms into half spectra and store rows k in [0, nts]
+// for all kP pairs of the block; consecutive threads take consecutive pairs of
+// one row (float4 each when aligned). The theta Nyquist row is zeroed.
 template <class F>
-__device__ __forceinline__ void store_half_spectra(const float2* a, int L, int nts, int n_rho, int l0,
+__device__ __forceinline__ void store_half_spectra(const float2* const* res, int L, int nts, int n_rho, int l0,
                                                    float2* __restrict__ out) {
-    for (int k = threadIdx.x; k <= nts; k += blockDim.x) {
+    constexpr int P = F::kP;
+    for (int e = threadIdx.x; e < (nts + 1) * P; e += blockDim.x) {
+        const int k = e / P, p = e % P;
+        const int l = l0 + 2 * p;
+        if (l >= n_rho) continue;
         float2 A = make_float2(0.f, 0.f), B = A;
         if (k < nts) {
-            const float2 z = a[F::idx(k)], zm = a[F::idx(k == 0 ? 0 : L - k)];
+            const float2 z = res[p][F::idx(k)], zm = res[p][F::idx(k == 0 ? 0 : L - k)];
             A = make_float2(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y));
             B = make_float2(0.5f * (z.y + zm.y), -0.5f * (z.x - zm.x));
         }
-        float2* row = out + size_t(k) * n_rho;
-        if (l0 + 1 < n_rho && ((size_t(k) * n_rho + l0) & 1) == 0) {
-            *reinterpret_cast<float4*>(row + l0) = make_float4(A.x, A.y, B.x, B.y);
+        float2* dst = out + size_t(k) * n_rho + l;
+        if (l + 1 < n_rho && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            *reinterpret_cast<float4*>(dst) = make_float4(A.x, A.y, B.x, B.y);
         } else {
-            row[l0] = A;
-            if (l0 + 1 < n_rho) row[l0 + 1] = B;
+            dst[0] = A;
+            if (l + 1 < n_rho) dst[1] = B;
         }
     }
 }
 
-// Load the half spectra of columns l0, l0 + 1 (k in [0, kmax)) and rebuild
-// the packed Hermitian transform of length L: Z(k) = A + iB, Z(L-k) = conj(A) + i conj(B).
+// Load half spectra rows k in [0, kmax) of the block's pairs and rebuild each
+// packed Hermitian transform of length L: Z(k) = A + iB, Z(L-k) = conj(A) + i conj(B).
 template <class F>
-__device__ __forceinline__ void load_packed_hermitian(float2* sm, const float2* __restrict__ in, int kmax, int L,
-                                                      int n, int l0) {
-    const bool two = l0 + 1 < n;
-    for (int k = threadIdx.x; k < kmax; k += blockDim.x) {
-        const float2* p = in + size_t(k) * n + l0;
+__device__ __forceinline__ void load_packed_hermitian(float2* const* sm, const float2* __restrict__ in, int kmax,
+                                                      int L, int n, int l0) {
+    constexpr int P = F::kP;
+    for (int e = threadIdx.x; e < kmax * P; e += blockDim.x) {
+        const int k = e / P, p = e % P;
+        const int l = l0 + 2 * p;
+        if (l >= n) continue;
+        const float2* src = in + size_t(k) * n + l;
         float2 A, B;
-        if (two && ((size_t(k) * n + l0) & 1) == 0) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        if (l + 1 < n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(src));
             A = make_float2(v.x, v.y);
             B = make_float2(v.z, v.w);
         } else {
-            A = p[0];
-            B = two ? p[1] : make_float2(0.f, 0.f);
+            A = src[0];
+            B = l + 1 < n ? src[1] : make_float2(0.f, 0.f);
         }
-        sm[F::idx(k)] = make_float2(A.x - B.y, A.y + B.x);
-        if (k > 0) sm[F::idx(L - k)] = make_float2(A.x + B.y, B.x - A.y);
+        sm[p][F::idx(k)] = make_float2(A.x - B.y, A.y + B.x);
+        if (k > 0) sm[p][F::idx(L - k)] = make_float2(A.x + B.y, B.x - A.y);
     }
 }
 
@@ -192,41 +224,55 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const float* __r
 
 // Alg. 1 steps 3-6a: gather T_m f e^rho on the fine grid of two rho columns,
 // zero-embed into the doubled fine period Lf, real theta FFT, keep |k| < nts.
+// Each thread gathers two fine rows per iteration (64 independent tap loads
+// in flight) to hide the L2 latency of the spline taps.
 template <class F>
-__global__ void __launch_bounds__(512) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                                         const float* __restrict__ qf, float2* __restrict__ spec) {
-    extern __shared__ float2 sm[];
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
+__global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                            const float* __restrict__ qf, float2* __restrict__ spec) {
+    extern __shared__ float2 smem[];
+    const Group<F> G;
+    const int E = F::elems(fd);
+    float2* sm = smem + G.g * E;
+    const int m = blockIdx.y, b = blockIdx.z;
+    const int l0b = 2 * F::kP * blockIdx.x, l0 = l0b + 2 * G.g;
     const int Lf = g.Lf, nf = g.nf;
-    for (int i = tid; i < Lf / 4; i += T) {  // the zero half [nf/2, Lf - nf/2)
+    for (int i = G.tid; i < Lf / 4; i += G.size) {  // the zero half [nf/2, Lf - nf/2)
         sm[F::idx(nf / 2 + i)] = make_float2(0.f, 0.f);
         sm[F::idx(nf / 2 + Lf / 4 + i)] = make_float2(0.f, 0.f);
     }
     const float* q = qf + size_t(b) * g.pitch * g.pitch;
     const float cm = g.cosm[m], smm = g.sinm[m];
-    const float er0 = __ldg(g.erho + l0);
-    const bool two = l0 + 1 < g.n_rho;
+    const bool one = l0 < g.n_rho, two = l0 + 1 < g.n_rho;
+    const float er0 = one ? __ldg(g.erho + l0) : 0.f;
     const float er1 = two ? __ldg(g.erho + l0 + 1) : 0.f;
-    for (int i = tid; i < nf; i += T) {
+    const int half_rows = nf / 2;
+    for (int i = G.tid; i < half_rows; i += G.size) {
+        const int i2 = i + half_rows;
         const float ct = __ldg(g.fine_cos + i), st = __ldg(g.fine_sin + i);
-        const float h0 = gather_image(g, q, cm, smm, er0, ct, st);
+        const float ct2 = __ldg(g.fine_cos + i2), st2 = __ldg(g.fine_sin + i2);
+        const float h0 = one ? gather_image(g, q, cm, smm, er0, ct, st) : 0.f;
         const float h1 = two ? gather_image(g, q, cm, smm, er1, ct, st) : 0.f;
-        const int qq = i - nf / 2;
-        sm[F::idx(qq < 0 ? qq + Lf : qq)] = make_float2(h0, h1);
+        const float h2 = one ? gather_image(g, q, cm, smm, er0, ct2, st2) : 0.f;
+        const float h3 = two ? gather_image(g, q, cm, smm, er1, ct2, st2) : 0.f;
+        sm[F::idx(i - nf / 2 + Lf)] = make_float2(h0, h1);  // q = i - nf/2 < 0
+        sm[F::idx(i2 - nf / 2)] = make_float2(h2, h3);      // q = i2 - nf/2 >= 0
     }
     __syncthreads();
-    const float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd);
+    float2* res[F::kP];
+    res[G.g] = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
+    __shared__ float2* rptr[F::kP];
+    if (G.tid == 0) rptr[G.g] = res[G.g];
+    __syncthreads();
     float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
-    store_half_spectra<F>(res, Lf, g.nts, g.n_rho, l0, out);
+    store_half_spectra<F>(rptr, Lf, g.nts, g.n_rho, l0b, out);
 }
 
 // rho pass: for every (item, k_theta) row, FFT along rho, multiply by the
-// kernel spectrum row, inverse FFT. One block per row; the multiplier row is
-// shared by all items of the batch (grid.y).
+// kernel spectrum row, inverse FFT. One transform per block; the multiplier
+// row is shared by all items of the batch (grid.y).
 template <class F>
-__global__ void __launch_bounds__(512) k_rho_pass(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                                  const float2* __restrict__ mult, float2* __restrict__ spec) {
+__global__ void LPR_LB(F) k_rho_pass(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                     const float2* __restrict__ mult, float2* __restrict__ spec) {
     extern __shared__ float2 sm[];
     const int tid = threadIdx.x, T = blockDim.x;
     const int k = blockIdx.x, item = blockIdx.y;
@@ -234,37 +280,49 @@ __global__ void __launch_bounds__(512) k_rho_pass(const __grid_constant__ DevGeo
     float2* row = spec + (size_t(item) * (g.nts + 1) + k) * n;
     for (int j = tid; j < n; j += T) sm[F::idx(j)] = row[j];
     __syncthreads();
-    float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd);
+    float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, tid);
     const float2* mrow = mult + size_t(k) * n;
     for (int j = tid; j < n; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], __ldg(mrow + j));
     __syncthreads();
-    a = F::template run<true>(a, a == sm ? fft_scratch<F>(sm, fd) : sm, fd);
+    a = F::template run<true>(a, a == sm ? fft_scratch<F>(sm, fd) : sm, fd, tid);
     for (int j = tid; j < n; j += T) row[j] = a[F::idx(j)];
 }
 
 // Hermitian theta inverse: two real columns per complex transform of length
 // 2 nts; rows [j0, j0 + win) of the periodic result are kept.
 template <class F>
-__global__ void __launch_bounds__(512) k_theta_inv(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                                   const float2* __restrict__ spec, float* __restrict__ lp) {
-    extern __shared__ float2 sm[];
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
+__global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                      const float2* __restrict__ spec, float* __restrict__ lp) {
+    extern __shared__ float2 smem[];
+    constexpr int P = F::kP;
+    const Group<F> G;
+    const int E = F::elems(fd);
+    float2* sms[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) sms[p] = smem + p * E;
+    const int m = blockIdx.y, b = blockIdx.z;
+    const int l0b = 2 * P * blockIdx.x;
     const int nts = g.nts, L2 = g.L2, n = g.n_rho;
-    const bool two = l0 + 1 < n;
     const size_t item = size_t(b) * g.M + m;
-    if (tid == 0) sm[F::idx(nts)] = make_float2(0.f, 0.f);  // Nyquist bin (zeroed band edge)
-    load_packed_hermitian<F>(sm, spec + item * size_t(nts + 1) * n, nts, L2, n, l0);
+    if (threadIdx.x < P) sms[threadIdx.x][F::idx(nts)] = make_float2(0.f, 0.f);  // zeroed band edge
+    load_packed_hermitian<F>(sms, spec + item * size_t(nts + 1) * n, nts, L2, n, l0b);
     __syncthreads();
-    const float2* res = F::template run<true>(sm, fft_scratch<F>(sm, fd), fd);
+    float2* res = F::template run<true>(sms[G.g], fft_scratch<F>(sms[G.g], fd), fd, G.tid);
+    __shared__ float2* rptr[P];
+    if (G.tid == 0) rptr[G.g] = res;
+    __syncthreads();
     float* out = lp + item * size_t(g.win) * n;
-    for (int r = tid; r < g.win; r += T) {
-        const float2 z = res[F::idx(wrapi(g.j0 + r, L2))];
-        if (two && ((size_t(r) * n + l0) & 1) == 0) {
-            *reinterpret_cast<float2*>(out + size_t(r) * n + l0) = z;
+    for (int e = threadIdx.x; e < g.win * P; e += blockDim.x) {
+        const int r = e / P, p = e % P;
+        const int l = l0b + 2 * p;
+        if (l >= n) continue;
+        const float2 z = rptr[p][F::idx(wrapi(g.j0 + r, L2))];
+        float* dst = out + size_t(r) * n + l;
+        if (l + 1 < n && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+            *reinterpret_cast<float2*>(dst) = z;
         } else {
-            out[size_t(r) * n + l0] = z.x;
-            if (two) out[size_t(r) * n + l0 + 1] = z.y;
+            dst[0] = z.x;
+            if (l + 1 < n) dst[1] = z.y;
         }
     }
 }
@@ -326,18 +384,21 @@ __device__ __forceinline__ float gather_sino(const float* __restrict__ row, int 
 // sample is a 1-D spline along s (zero outside the detector), then the real
 // theta FFT of the zero-embedded doubled period.
 template <class F>
-__global__ void __launch_bounds__(512) k_bp_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                                      const float* __restrict__ qg, float2* __restrict__ spec) {
-    extern __shared__ float2 sm[];
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
+__global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                         const float* __restrict__ qg, float2* __restrict__ spec) {
+    extern __shared__ float2 smem[];
+    const Group<F> G;
+    const int E = F::elems(fd);
+    float2* sm = smem + G.g * E;
+    const int m = blockIdx.y, b = blockIdx.z;
+    const int l0b = 2 * F::kP * blockIdx.x, l0 = l0b + 2 * G.g;
     const int nts = g.nts, L2 = g.L2, N = g.N;
-    for (int i = tid; i < nts; i += T) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
-    const bool two = l0 + 1 < g.n_rho;
-    const float er0 = __ldg(g.erho + l0);
+    for (int i = G.tid; i < nts; i += G.size) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
+    const bool one = l0 < g.n_rho, two = l0 + 1 < g.n_rho;
+    const float er0 = one ? __ldg(g.erho + l0) : 0.f;
     const float er1 = two ? __ldg(g.erho + l0 + 1) : 0.f;
     const float halfN = 0.5f * N;
-    for (int jj = tid; jj < nts; jj += T) {
+    for (int jj = G.tid; jj < nts; jj += G.size) {
         const int j = jj - nts / 2;
         int i = m * nts + j;
         const bool flip = i < 0;
@@ -346,67 +407,85 @@ __global__ void __launch_bounds__(512) k_bp_theta_fwd(const __grid_constant__ De
         const float cth = __ldg(g.coarse_cos + jj) * g.one_m_aR;
         const float sg = flip ? -halfN : halfN;
         // t = (s_raster + 1/2) N with s_raster = (e^rho - (1-aR) cos) / (2 aR)
-        const float t0 = fmaf((er0 - cth) * g.inv_aR, sg, halfN);
-        const float v0 = gather_sino(row, N, t0);
-        float v1 = 0.f;
-        if (two) v1 = gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN));
+        const float v0 = one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN)) : 0.f;
+        const float v1 = two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN)) : 0.f;
         sm[F::idx(j < 0 ? j + L2 : j)] = make_float2(v0, v1);
     }
     __syncthreads();
-    const float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd);
+    float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
+    __shared__ float2* rptr[F::kP];
+    if (G.tid == 0) rptr[G.g] = res;
+    __syncthreads();
     float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * g.n_rho;
-    store_half_spectra<F>(res, L2, nts, g.n_rho, l0, out);
+    store_half_spectra<F>(rptr, L2, nts, g.n_rho, l0b, out);
 }
 
 // R^T stage 2: real theta FFT of the lattice rows [-nts/2, nts/2) held in
 // the window buffer (the transpose of the forward theta inverse + crop).
 template <class F>
-__global__ void __launch_bounds__(512) k_theta_fwd_T(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                                     const float* __restrict__ lp, float2* __restrict__ spec) {
-    extern __shared__ float2 sm[];
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
+__global__ void LPR_LB(F) k_theta_fwd_T(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                        const float* __restrict__ lp, float2* __restrict__ spec) {
+    extern __shared__ float2 smem[];
+    constexpr int P = F::kP;
+    const Group<F> G;
+    const int E = F::elems(fd);
+    const int m = blockIdx.y, b = blockIdx.z;
+    const int l0b = 2 * P * blockIdx.x;
     const int nts = g.nts, L2 = g.L2, n = g.n_rho;
-    const bool two = l0 + 1 < n;
-    for (int i = tid; i < nts; i += T) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
+    {
+        float2* sm = smem + G.g * E;
+        for (int i = G.tid; i < nts; i += G.size) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
+    }
     const float* in = lp + (size_t(b) * g.M + m) * size_t(g.win) * n;
-    for (int jj = tid; jj < nts; jj += T) {
+    for (int e = threadIdx.x; e < nts * P; e += blockDim.x) {
+        const int jj = e / P, p = e % P;
+        const int l = l0b + 2 * p;
         const int j = jj - nts / 2;
         const float* row = in + size_t(j - g.j0) * n;
-        sm[F::idx(j < 0 ? j + L2 : j)] = make_float2(row[l0], two ? row[l0 + 1] : 0.f);
+        const float a = l < n ? row[l] : 0.f, c = l + 1 < n ? row[l + 1] : 0.f;
+        smem[p * E + F::idx(j < 0 ? j + L2 : j)] = make_float2(a, c);
     }
     __syncthreads();
-    const float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd);
+    float2* sm = smem + G.g * E;
+    float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
+    __shared__ float2* rptr[P];
+    if (G.tid == 0) rptr[G.g] = res;
+    __syncthreads();
     float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * n;
-    store_half_spectra<F>(res, L2, nts, n, l0, out);
+    store_half_spectra<F>(rptr, L2, nts, n, l0b, out);
 }
 
 // R^T stage 4: Hermitian inverse over the doubled fine period (zero beyond
 // |k| < nts) and the transposed fine-grid gather G_m^T, scattering the spline
 // taps into the apron-extended coefficient image.
 template <class F>
-__global__ void __launch_bounds__(512) k_theta_inv_fine_T(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                                          const float2* __restrict__ spec, float* __restrict__ qbar) {
-    extern __shared__ float2 sm[];
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int l0 = 2 * blockIdx.x, m = blockIdx.y, b = blockIdx.z;
+__global__ void LPR_LB(F) k_theta_inv_fine_T(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                             const float2* __restrict__ spec, float* __restrict__ qbar) {
+    extern __shared__ float2 smem[];
+    constexpr int P = F::kP;
+    const Group<F> G;
+    const int E = F::elems(fd);
+    float2* sms[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) sms[p] = smem + p * E;
+    const int m = blockIdx.y, b = blockIdx.z;
+    const int l0b = 2 * P * blockIdx.x, l0 = l0b + 2 * G.g;
     const int nts = g.nts, Lf = g.Lf, n = g.n_rho, nf = g.nf;
-    const bool two = l0 + 1 < n;
     const size_t item = size_t(b) * g.M + m;
-    for (int k = nts + tid; k <= Lf - nts; k += T) sm[F::idx(k)] = make_float2(0.f, 0.f);
-    load_packed_hermitian<F>(sm, spec + item * size_t(nts + 1) * n, nts, Lf, n, l0);
+    for (int k = nts + G.tid; k <= Lf - nts; k += G.size) sms[G.g][F::idx(k)] = make_float2(0.f, 0.f);
+    load_packed_hermitian<F>(sms, spec + item * size_t(nts + 1) * n, nts, Lf, n, l0b);
     __syncthreads();
-    const float2* res = F::template run<true>(sm, fft_scratch<F>(sm, fd), fd);
+    const float2* res = F::template run<true>(sms[G.g], fft_scratch<F>(sms[G.g], fd), fd, G.tid);
     float* q = qbar + size_t(b) * g.pitch * g.pitch;
     const float cm = g.cosm[m], smm = g.sinm[m];
     const float half = 0.5f * g.N;
-    for (int i = tid; i < nf; i += T) {
+    for (int i = G.tid; i < nf; i += G.size) {
         const int qq = i - nf / 2;
         const float2 z = res[F::idx(qq < 0 ? qq + Lf : qq)];
         const float ct = __ldg(g.fine_cos + i), st = __ldg(g.fine_sin + i);
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            if (c == 1 && !two) break;
+            if (l0 + c >= n) break;
             const float er = __ldg(g.erho + l0 + c);
             const float dx = fmaf(er, ct, -g.one_m_aR), dy = er * st;
             if (fmaf(dx, dx, dy * dy) > g.aR2) continue;
@@ -476,10 +555,12 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
 
 // ------------------------------------------------------------- host launchers
 FftLaunch fft_launch_config(const FftDesc& d) {
-    FftLaunch L{kFftGeneric, GenericFft::threads(d), size_t(GenericFft::elems(d)) * sizeof(float2)};
+    const int gt = GenericFft::threads(d);
+    FftLaunch L{kFftGeneric, gt, gt, 1, size_t(GenericFft::elems(d)) * sizeof(float2)};
     if (d.nb != 0) return L;
-#define LPR_PICK(F, ID)                                                          \
-    if (d.n == F::kN) return FftLaunch{ID, F::kT, size_t(F::elems(d)) * sizeof(float2)};
+#define LPR_PICK(F, ID)                                                                                     \
+    if (d.n == F::kN)                                                                                       \
+        return FftLaunch{ID, F::kT * F::kP, F::kT, F::kP, size_t(F::elems(d)) * sizeof(float2)};
     LPR_PICK(Fft2048, kFft2048)
     LPR_PICK(Fft4096, kFft4096)
     LPR_PICK(Fft4374, kFft4374)
@@ -499,6 +580,12 @@ FftLaunch fft_launch_config(const FftDesc& d) {
         default: CALL(GenericFft); break;      \
     }
 
+// grid.x arrives as the number of column pairs; a block takes per_block of them
+static dim3 theta_grid(dim3 grid, const FftLaunch& L) {
+    grid.x = (grid.x + L.per_block - 1) / L.per_block;
+    return grid;
+}
+
 static cudaError_t smem_attr(const void* fn, size_t bytes) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
@@ -507,12 +594,15 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
     cudaError_t e = cudaSuccess;
 #define SET(K, L)                                                              \
     do {                                                                       \
-        cudaError_t r = smem_attr((const void*)K, L.smem);                     \
+        cudaError_t r = smem_attr((const void*)K, L);                          \
         if (r != cudaSuccess) e = r;                                           \
     } while (0)
-#define FINE(F) SET(k_radon_theta_fwd<F>, fine); SET(k_theta_inv_fine_T<F>, fine)
-#define RHO(F) SET(k_rho_pass<F>, rho)
-#define COARSE(F) SET(k_theta_inv<F>, coarse); SET(k_bp_theta_fwd<F>, coarse); SET(k_theta_fwd_T<F>, coarse)
+#define FINE(F) SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block); SET(k_theta_inv_fine_T<F>, fine.smem * fine.per_block)
+#define RHO(F) SET(k_rho_pass<F>, rho.smem)
+#define COARSE(F)                                          \
+    SET(k_theta_inv<F>, coarse.smem * coarse.per_block);    \
+    SET(k_bp_theta_fwd<F>, coarse.smem * coarse.per_block); \
+    SET(k_theta_fwd_T<F>, coarse.smem * coarse.per_block)
     LPR_FFT_SWITCH(fine.variant, FINE)
     LPR_FFT_SWITCH(rho.variant, RHO)
     LPR_FFT_SWITCH(coarse.variant, COARSE)
@@ -525,42 +615,42 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                             const float* qf, float2* spec) {
-#define CALL(F) k_radon_theta_fwd<F><<<grid, L.threads, L.smem, st>>>(g, fd, qf, spec)
+#define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }
 
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec) {
-#define CALL(F) k_rho_pass<F><<<grid, L.threads, L.smem, st>>>(g, fd, mult, spec)
+#define CALL(F) k_rho_pass<F><<<grid, L.tpt, L.smem, st>>>(g, fd, mult, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }
 
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                       const float2* spec, float* lp) {
-#define CALL(F) k_theta_inv<F><<<grid, L.threads, L.smem, st>>>(g, fd, spec, lp)
+#define CALL(F) k_theta_inv<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, spec, lp)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }
 
 void launch_bp_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                          const float* qg, float2* spec) {
-#define CALL(F) k_bp_theta_fwd<F><<<grid, L.threads, L.smem, st>>>(g, fd, qg, spec)
+#define CALL(F) k_bp_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qg, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }
 
 void launch_theta_fwd_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                         const float* lp, float2* spec) {
-#define CALL(F) k_theta_fwd_T<F><<<grid, L.threads, L.smem, st>>>(g, fd, lp, spec)
+#define CALL(F) k_theta_fwd_T<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, lp, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }
 
 void launch_theta_inv_fine_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                              const float2* spec, float* qbar) {
-#define CALL(F) k_theta_inv_fine_T<F><<<grid, L.threads, L.smem, st>>>(g, fd, spec, qbar)
+#define CALL(F) k_theta_inv_fine_T<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, spec, qbar)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }

@@ -36,8 +36,10 @@ struct DevGeom {
 enum FftVariant : int { kFftGeneric = 0, kFft2048, kFft4096, kFft4374, kFft8192, kFft16384 };
 struct FftLaunch {
     int variant;
-    int threads;
-    size_t smem;
+    int threads;   // block size of the theta kernels (kT * kP)
+    int tpt;       // threads per transform (block size of the rho pass)
+    int per_block; // transforms (column pairs) per theta block
+    size_t smem;   // shared bytes of one transform
 };
 
 // host-side launchers (lpr_kernels.cu)

@@ -151,12 +151,8 @@ def fast_backprojection(sino, plan: RadonPlan):
 def radon_transpose(sino, plan: RadonPlan):
     """Exact adjoint of fast_radon under the weighted inner products of adjoint_gap."""
     g = plan.geometry
-    if not _is_torch(sino):
-        import torch
-
-        t = torch.as_tensor(np.ascontiguousarray(sino, dtype=np.float32), device=f"cuda:{plan.device}")
-        return radon_transpose(t, plan).cpu().numpy()
-    return _run(plan, sino, (g.n_theta, g.N), (g.N, g.N), lib().lpr_gpu_radon_transpose, None)
+    return _run(plan, sino, (g.n_theta, g.N), (g.N, g.N), lib().lpr_gpu_radon_transpose,
+                lib().lpr_gpu_radon_transpose_host)
 
 
 def inner_sinogram(g: Geometry, a, b) -> float:

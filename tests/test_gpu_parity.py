@@ -174,3 +174,17 @@ def test_exact_transpose_adjoint_identity(lp, lpo, cuda, N):
 def test_adjoint_gap_exact_gpu(lp, lpo, cuda):
     g, p, z, zb, plan = _setup(lp, lpo, 64)
     assert lp.adjoint_gap(plan, trials=5, exact=True) <= 1e-5
+
+
+def test_cpp_dropin_against_reference_blocks(cuda):
+    """The C++ drop-in (include/lpradon/lp_ops.hpp) driven by the reference's own
+    compiled sampling_plan / zeta_spectrum / direct oracles (tests/dropin)."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "paper_1506_00014_b200", "_dropin", "dropin_smoke")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in driver not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "adjoint gap" in r.stdout
