@@ -209,7 +209,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1506_00014_b200 as lp
-    from paper_1506_00014_b200 import phantoms, roofline
+    from paper_1506_00014_b200 import phantoms, roofline, sharding
+    from paper_1506_00014_b200.sharding import stack_shard
 
     rank, ws, local = world()
     torch.cuda.set_device(local)
@@ -220,7 +221,9 @@ def run_ours(args):
     z, zb = lp.zeta_spectrum(g), lp.zeta_bp_spectrum(g)
     B = args.batch
     plan = lp.RadonPlan(g, z, zb, max_batch=B, device=local)
-    imgs = phantoms.stack(g.N, B, seed0=0x5EED + rank * B, device=dev)
+    start, count = stack_shard(B * ws, ws, rank)  # this rank's slices of the stack (weak scaling)
+    assert count == B
+    imgs = phantoms.stack(g.N, B, seed0=0x5EED + start, device=dev)
     sino = torch.empty(B, g.n_theta, g.N, device=dev)
     back = torch.empty(B, g.N, g.N, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -237,11 +240,7 @@ def run_ours(args):
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if ws == 1:
-            return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return sharding.max_over_ranks(x, device=dev)
 
     for _ in range(max(args.warmup, 3)):
         step()

@@ -25,7 +25,19 @@ int main() {
     const int N = 64;
     const lpr::GeometryPlan geom = lpr::sampling_plan(N, 3);
     const lpr::RadonPlan plan = lpr::make_radon_plan(geom);
-    const lpr::Image f = lpr::phantom_image(N);
+    // SPEC.md:570 uses smooth random images; a smooth two-blob disc image here
+    // (the sharp Shepp-Logan phantom is 6.5% off even for direct_radon at N=64).
+    lpr::Image f;
+    f.grid = geom.cartesian_grid();
+    f.pixels = lpr::Array2D<double>(N, N);
+    for (int r = 0; r < N; ++r)
+        for (int c = 0; c < N; ++c) {
+            const double x = -0.5 + double(c) / N, y = -0.5 + double(r) / N;
+            const double rr = std::sqrt(x * x + y * y);
+            const double taper = rr < 0.38 ? 1.0 : (rr < 0.45 ? 0.5 * (1 + std::cos(M_PI * (rr - 0.38) / 0.07)) : 0.0);
+            f.pixels(r, c) = taper * (std::exp(-((x - 0.1) * (x - 0.1) + (y + 0.05) * (y + 0.05)) / 0.01) +
+                                      0.6 * std::exp(-((x + 0.12) * (x + 0.12) + (y - 0.1) * (y - 0.1)) / 0.005));
+        }
     const lpr::Sinogram fast = lpr::fast_radon(f, plan);
     const lpr::Sinogram direct = lpr::direct_radon(f, geom.polar_grid());
     const double e_r = rel_l2(fast.values, direct.values);
