@@ -181,7 +181,7 @@ struct lpr_gpu_plan {
             d.bhat = upload(bh);
         }
         launch = fft_launch_config(d);
-        if (launch.smem * launch.per_block > 227 * 1024)
+        if (launch.smem * launch.per_block > 227 * 1024 || launch.smem + size_t(n) * sizeof(float2) > 227 * 1024)
             throw std::invalid_argument("fft: transform does not fit in shared memory");
     }
 
@@ -330,7 +330,8 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     ck(cudaHostAlloc(&p->h_out, io * sizeof(float), cudaHostAllocDefault), "cudaHostAlloc");
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
 
-    ck(prepare_fft_kernels(p->l_fine, p->l_rho, p->l_coarse), "fft smem attributes");
+    ck(prepare_fft_kernels(p->l_fine, p->l_rho, p->l_coarse, size_t(G.n_rho) * sizeof(float2)),
+       "fft smem attributes");
     set_smem((const void*)k_radon_out, size_t(nr) * sizeof(float));
     set_smem((const void*)k_radon_out_T, size_t(nr) * sizeof(float));
 

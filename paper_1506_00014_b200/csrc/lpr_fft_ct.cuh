@@ -5,7 +5,8 @@
 // registers between two barriers, with radices of 6..32 so a transform takes
 // 3-4 shared-memory round trips, and the index map pad(i) = i + i/16 keeps
 // the strided Stockham writes of the early passes (stride R float2) off
-// colliding banks.
+// colliding banks (the padding per length is chosen by a bank-conflict
+// count of each pass, see ct_pad).
 #pragma once
 
 #include "lpr_fft.cuh"
@@ -97,10 +98,15 @@ struct Dft<32, INV> {
     __device__ __forceinline__ static void run(float2* v) { dft_pq<4, 8, INV>(v); }
 };
 
-__host__ __device__ constexpr int ct_pad(int i) { return i + (i >> 4); }
+// Padded shared index: one spare slot every 2^S elements (S = 0: none). The
+// best S per plan comes from a bank-conflict count of every pass's read and
+// write pattern (64-bit accesses, half-warp phases): i/16 for 2048 and 4096,
+// i/32 for 8192 and 16384, none for 4374 (radix 6/9 strides).
+template <int S>
+__host__ __device__ constexpr int ct_pad(int i) { return S ? i + (i >> S) : i; }
 
 // One in-place pass of radix R at Stockham stride NS over a padded buffer.
-template <int N, int T, int R, int NS, bool INV>
+template <int N, int T, int S, int R, int NS, bool INV>
 __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw, int tid) {
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
@@ -111,7 +117,7 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
         const int b = tid + i * T;
         if (b < B) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[i][r] = x[ct_pad(b + r * B)];
+            for (int r = 0; r < R; ++r) v[i][r] = x[ct_pad<S>(b + r * B)];
         }
     }
     __syncthreads();
@@ -130,16 +136,16 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
             Dft<R, INV>::run(v[i]);
             const int base = (b - k) * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[ct_pad(base + r * NS)] = v[i][r];
+            for (int r = 0; r < R; ++r) x[ct_pad<S>(base + r * NS)] = v[i][r];
         }
     }
     __syncthreads();
 }
 
-template <int N, int T, bool INV, int NS, int R, int... Rest>
+template <int N, int T, int S, bool INV, int NS, int R, int... Rest>
 __device__ __forceinline__ void ct_run(float2* x, const float2* tw, int tid) {
-    ct_pass<N, T, R, NS, INV>(x, tw, tid);
-    if constexpr (sizeof...(Rest) > 0) ct_run<N, T, INV, NS * R, Rest...>(x, tw, tid);
+    ct_pass<N, T, S, R, NS, INV>(x, tw, tid);
+    if constexpr (sizeof...(Rest) > 0) ct_run<N, T, S, INV, NS * R, Rest...>(x, tw, tid);
 }
 
 // FFT policies: idx() (the buffer slot of element i), elems() (shared
@@ -148,17 +154,20 @@ __device__ __forceinline__ void ct_run(float2* x, const float2* tw, int tid) {
 // columns, so kP pairs make 4 kP contiguous columns per global row access),
 // kMinBlocks for __launch_bounds__, and run() on the calling thread group
 // (gtid in [0, kT); every thread of the block must call it).
-template <int N, int T, int P, int MINB, int... R>
+template <int N, int T, int P, int MINB, int S, int... R>
 struct CtFft {
     static constexpr int kN = N;
     static constexpr int kT = T;
     static constexpr int kP = P;
     static constexpr int kMinBlocks = MINB;
-    __device__ __forceinline__ static int idx(int i) { return ct_pad(i); }
-    __host__ __device__ static int elems(const FftDesc&) { return ct_pad(N - 1) + 1; }
+    // per-transform slots, rounded to 4 mod 16 so the kP buffers of a block
+    // start on different banks (row loads spread consecutive lanes over them)
+    static constexpr int kElems = (ct_pad<S>(N - 1) + 1 + 12) / 16 * 16 + 4;
+    __device__ __forceinline__ static int idx(int i) { return ct_pad<S>(i); }
+    __host__ __device__ static int elems(const FftDesc&) { return kElems; }
     template <bool INV>
     __device__ __forceinline__ static float2* run(float2* x, float2*, const FftDesc& d, int gtid) {
-        ct_run<N, T, INV, 1, R...>(x, d.tw, gtid);
+        ct_run<N, T, S, INV, 1, R...>(x, d.tw, gtid);
         return x;
     }
 };
@@ -182,11 +191,11 @@ struct GenericFft {
 };
 
 // The compile-time shapes, by length (host-side selection in lpr_capi.cu).
-//                   N      T   P  minB  radices
-using Fft2048 = CtFft<2048, 128, 4, 2, 16, 16, 8>;
-using Fft4096 = CtFft<4096, 256, 2, 1, 16, 16, 16>;
-using Fft4374 = CtFft<4374, 256, 1, 3, 6, 9, 9, 9>;
-using Fft8192 = CtFft<8192, 256, 1, 2, 32, 16, 16>;
-using Fft16384 = CtFft<16384, 512, 1, 1, 32, 32, 16>;
+//                   N      T   P  minB pad radices
+using Fft2048 = CtFft<2048, 128, 4, 2, 4, 16, 16, 8>;
+using Fft4096 = CtFft<4096, 256, 2, 1, 4, 16, 16, 16>;
+using Fft4374 = CtFft<4374, 256, 1, 3, 0, 6, 9, 9, 9>;
+using Fft8192 = CtFft<8192, 256, 1, 2, 5, 32, 16, 16>;
+using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 
 }  // namespace lpr

@@ -11,6 +11,8 @@
 //       k_radon_out        S_m resampling to the sinogram, a_R^-1 (step 7)
 //   R#: k_prefilter_sino -> k_bp_theta_fwd -> k_rho_pass -> k_theta_inv
 //       -> k_bp_out (sector sum in ascending m, x2)
+#include <cuda_pipeline.h>
+
 #include <cstdint>
 
 #include "lpr_fft_ct.cuh"
@@ -177,25 +179,44 @@ __device__ __forceinline__ void store_half_spectra(const float2* const* res, int
 // Load half spectra rows k in [0, kmax) of the block's pairs and rebuild each
 // packed Hermitian transform of length L: Z(k) = A + iB, Z(L-k) = conj(A) + i conj(B).
 template <class F>
+__device__ __forceinline__ void put_packed(float2* const* sm, int k, int p, int L, float2 A, float2 B) {
+    sm[p][F::idx(k)] = make_float2(A.x - B.y, A.y + B.x);
+    if (k > 0) sm[p][F::idx(L - k)] = make_float2(A.x + B.y, B.x - A.y);
+}
+
+template <class F>
 __device__ __forceinline__ void load_packed_hermitian(float2* const* sm, const float2* __restrict__ in, int kmax,
                                                       int L, int n, int l0) {
     constexpr int P = F::kP;
-    for (int e = threadIdx.x; e < kmax * P; e += blockDim.x) {
+    constexpr int U = 8;  // independent 16-byte loads in flight per thread
+    const int total = kmax * P;
+    const bool vec = l0 + 2 * P <= n && (n % 2) == 0 && (reinterpret_cast<uintptr_t>(in + l0) & 15) == 0;
+    if (vec) {
+        for (int base = threadIdx.x; base < total; base += U * blockDim.x) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = base + u * blockDim.x;
+                if (e < total)
+                    v[u] = __ldg(reinterpret_cast<const float4*>(in + size_t(e / P) * n + l0 + 2 * (e % P)));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = base + u * blockDim.x;
+                if (e < total)
+                    put_packed<F>(sm, e / P, e % P, L, make_float2(v[u].x, v[u].y), make_float2(v[u].z, v[u].w));
+            }
+        }
+        return;
+    }
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
         const int k = e / P, p = e % P;
         const int l = l0 + 2 * p;
         if (l >= n) continue;
         const float2* src = in + size_t(k) * n + l;
-        float2 A, B;
-        if (l + 1 < n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(src));
-            A = make_float2(v.x, v.y);
-            B = make_float2(v.z, v.w);
-        } else {
-            A = src[0];
-            B = l + 1 < n ? src[1] : make_float2(0.f, 0.f);
-        }
-        sm[p][F::idx(k)] = make_float2(A.x - B.y, A.y + B.x);
-        if (k > 0) sm[p][F::idx(L - k)] = make_float2(A.x + B.y, B.x - A.y);
+        const float2 A = src[0];
+        const float2 B = l + 1 < n ? src[1] : make_float2(0.f, 0.f);
+        put_packed<F>(sm, k, p, L, A, B);
     }
 }
 
@@ -268,8 +289,10 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
 }
 
 // rho pass: for every (item, k_theta) row, FFT along rho, multiply by the
-// kernel spectrum row, inverse FFT. One transform per block; the multiplier
-// row is shared by all items of the batch (grid.y).
+// kernel spectrum row, inverse FFT. One transform per block. The row and the
+// multiplier row are staged with cp.async (LDGSTS): the row is awaited before
+// the forward FFT, the multiplier lands during it. The multiplier rows are
+// shared by all items of the batch (grid.y), so they stay L2-resident.
 template <class F>
 __global__ void LPR_LB(F) k_rho_pass(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                      const float2* __restrict__ mult, float2* __restrict__ spec) {
@@ -277,12 +300,19 @@ __global__ void LPR_LB(F) k_rho_pass(const __grid_constant__ DevGeom g, const __
     const int tid = threadIdx.x, T = blockDim.x;
     const int k = blockIdx.x, item = blockIdx.y;
     const int n = g.n_rho;
+    float2* ms = sm + F::elems(fd);
     float2* row = spec + (size_t(item) * (g.nts + 1) + k) * n;
-    for (int j = tid; j < n; j += T) sm[F::idx(j)] = row[j];
+    const float2* mrow = mult + size_t(k) * n;
+    for (int j = tid; j < n; j += T) __pipeline_memcpy_async(sm + F::idx(j), row + j, sizeof(float2));
+    __pipeline_commit();
+    for (int j = tid; j < n; j += T) __pipeline_memcpy_async(ms + j, mrow + j, sizeof(float2));
+    __pipeline_commit();
+    __pipeline_wait_prior(1);
     __syncthreads();
     float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, tid);
-    const float2* mrow = mult + size_t(k) * n;
-    for (int j = tid; j < n; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], __ldg(mrow + j));
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    for (int j = tid; j < n; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], ms[j]);
     __syncthreads();
     a = F::template run<true>(a, a == sm ? fft_scratch<F>(sm, fd) : sm, fd, tid);
     for (int j = tid; j < n; j += T) row[j] = a[F::idx(j)];
@@ -398,18 +428,27 @@ __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, cons
     const float er0 = one ? __ldg(g.erho + l0) : 0.f;
     const float er1 = two ? __ldg(g.erho + l0 + 1) : 0.f;
     const float halfN = 0.5f * N;
-    for (int jj = G.tid; jj < nts; jj += G.size) {
-        const int j = jj - nts / 2;
-        int i = m * nts + j;
-        const bool flip = i < 0;
-        if (flip) i += g.n_theta;
-        const float* row = qg + (size_t(b) * g.n_theta + i) * N;
-        const float cth = __ldg(g.coarse_cos + jj) * g.one_m_aR;
-        const float sg = flip ? -halfN : halfN;
-        // t = (s_raster + 1/2) N with s_raster = (e^rho - (1-aR) cos) / (2 aR)
-        const float v0 = one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN)) : 0.f;
-        const float v1 = two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN)) : 0.f;
-        sm[F::idx(j < 0 ? j + L2 : j)] = make_float2(v0, v1);
+    // two lattice rows per iteration (jj and jj + nts/2) for more loads in flight
+    for (int jh = G.tid; jh < nts / 2; jh += G.size) {
+        float v[2][2];
+        int slot[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int jj = jh + h * (nts / 2);
+            const int j = jj - nts / 2;
+            int i = m * nts + j;
+            const bool flip = i < 0;
+            if (flip) i += g.n_theta;
+            const float* row = qg + (size_t(b) * g.n_theta + i) * N;
+            const float cth = __ldg(g.coarse_cos + jj) * g.one_m_aR;
+            const float sg = flip ? -halfN : halfN;
+            // t = (s_raster + 1/2) N with s_raster = (e^rho - (1-aR) cos) / (2 aR)
+            v[h][0] = one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN)) : 0.f;
+            v[h][1] = two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN)) : 0.f;
+            slot[h] = j < 0 ? j + L2 : j;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) sm[F::idx(slot[h])] = make_float2(v[h][0], v[h][1]);
     }
     __syncthreads();
     float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
@@ -590,7 +629,8 @@ static cudaError_t smem_attr(const void* fn, size_t bytes) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
-cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse) {
+cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
+                                size_t rho_mult_bytes) {
     cudaError_t e = cudaSuccess;
 #define SET(K, L)                                                              \
     do {                                                                       \
@@ -598,7 +638,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
         if (r != cudaSuccess) e = r;                                           \
     } while (0)
 #define FINE(F) SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block); SET(k_theta_inv_fine_T<F>, fine.smem * fine.per_block)
-#define RHO(F) SET(k_rho_pass<F>, rho.smem)
+#define RHO(F) SET(k_rho_pass<F>, rho.smem + rho_mult_bytes)
 #define COARSE(F)                                          \
     SET(k_theta_inv<F>, coarse.smem * coarse.per_block);    \
     SET(k_bp_theta_fwd<F>, coarse.smem * coarse.per_block); \
@@ -622,7 +662,7 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
 
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec) {
-#define CALL(F) k_rho_pass<F><<<grid, L.tpt, L.smem, st>>>(g, fd, mult, spec)
+#define CALL(F) k_rho_pass<F><<<grid, L.tpt, L.smem + size_t(g.n_rho) * sizeof(float2), st>>>(g, fd, mult, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }

@@ -44,7 +44,8 @@ struct FftLaunch {
 
 // host-side launchers (lpr_kernels.cu)
 FftLaunch fft_launch_config(const FftDesc& d);
-cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse);
+cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
+                                size_t rho_mult_bytes);
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                             const float* qf, float2* spec);
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
