@@ -181,6 +181,7 @@ struct lpr_gpu_plan {
             d.bhat = upload(bh);
         }
         launch = fft_launch_config(d);
+        if (launch.variant != kFftGeneric) d.twp = upload(fft_pass_twiddles(launch.variant));
         if (launch.smem * launch.per_block > 227 * 1024 || launch.smem + size_t(n) * sizeof(float2) > 227 * 1024)
             throw std::invalid_argument("fft: transform does not fit in shared memory");
     }
@@ -231,9 +232,12 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     g.inv_drho = float(1.0 / G.drho);
     g.inv_dtheta_p = float(1.0 / G.dtheta_p);
     g.out_scale = float(1.0 / (2.0 * G.a_R));
+    g.mask_k = float(1.0 - 2.0 * G.a_R);
     for (int m = 0; m < G.M; ++m) {
         g.cosm[m] = float(std::cos(m * G.beta));
         g.sinm[m] = float(std::sin(m * G.beta));
+        g.vcm[m] = float(0.5 * G.N * (1.0 - std::cos(m * G.beta) * (1.0 - G.a_R) / G.a_R));
+        g.vrm[m] = float(0.5 * G.N * (1.0 - std::sin(m * G.beta) * (1.0 - G.a_R) / G.a_R));
     }
     std::vector<float> fc(g.nf), fs(g.nf), cc(G.nts), er(G.n_rho), fir(2 * kFirHalf + 1);
     for (int i = 0; i < g.nf; ++i) {

@@ -23,7 +23,8 @@ struct FftDesc {
     int n = 0;
     int npass = 0;
     int radix[kMaxPasses] = {};
-    const float2* tw = nullptr;  // tw[j] = exp(-2 pi i j / n)
+    const float2* tw = nullptr;   // tw[j] = exp(-2 pi i j / n)
+    const float2* twp = nullptr;  // per-pass twiddles of the compile-time plan (lpr_fft_ct.cuh)
     // Bluestein: when nb > 0 the transform of length n runs through length nb
     int nb = 0;
     int nbpass = 0;
@@ -33,14 +34,19 @@ struct FftDesc {
     const float2* bhat = nullptr;  // FFT_nb of conj chirp kernel, times 1/nb
 };
 
+// Complex arithmetic on the sm_100 packed fp32x2 pipe (FADD2/FMUL2/FFMA2: one
+// instruction per complex add, two per complex multiply; IEEE per lane).
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+// a * b = a.x (b.x, b.y) + a.y (-b.y, b.x)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), b));
 }
-__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
-    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+// a * conj(b) = a.x (b.x, -b.y) + a.y (b.y, b.x)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), make_float2(b.x, -b.y)));
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 // multiply by -i (forward) or +i (inverse)
 template <bool INV>
@@ -134,8 +140,8 @@ struct DftOdd {
             for (int r = 1; r < R; ++r) {
                 const int k = (r * q) % R;
                 const float c = rt.c[k], s = INV ? rt.s[k] : -rt.s[k];
-                acc.x = fmaf(v[r].x, c, fmaf(-v[r].y, s, acc.x));
-                acc.y = fmaf(v[r].x, s, fmaf(v[r].y, c, acc.y));
+                acc = __ffma2_rn(make_float2(v[r].x, v[r].x), make_float2(c, s), acc);
+                acc = __ffma2_rn(make_float2(v[r].y, v[r].y), make_float2(-s, c), acc);
             }
             out[q] = acc;
         }
@@ -143,8 +149,21 @@ struct DftOdd {
         for (int q = 0; q < R; ++q) v[q] = out[q];
     }
 };
+// radix 3: X0 = v0 + t1, X1,2 = (v0 - t1/2) -/+ i (sqrt3/2) t2 (forward), t1 = v1 + v2, t2 = v1 - v2
 template <bool INV>
-struct Dft<3, INV> : DftOdd<3, INV> {};
+struct Dft<3, INV> {
+    __device__ __forceinline__ static void run(float2* v) {
+        constexpr float s = 0.86602540378443865f;
+        const float2 t1 = cadd(v[1], v[2]);
+        const float2 t2 = csub(v[1], v[2]);
+        const float2 m = __ffma2_rn(t1, make_float2(-0.5f, -0.5f), v[0]);
+        const float2 u = INV ? __fmul2_rn(make_float2(-t2.y, t2.x), make_float2(s, s))
+                             : __fmul2_rn(make_float2(t2.y, -t2.x), make_float2(s, s));
+        v[0] = cadd(v[0], t1);
+        v[1] = cadd(m, u);
+        v[2] = csub(m, u);
+    }
+};
 template <bool INV>
 struct Dft<5, INV> : DftOdd<5, INV> {};
 template <bool INV>

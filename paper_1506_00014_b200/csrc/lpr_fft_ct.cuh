@@ -9,6 +9,9 @@
 // count of each pass, see ct_pad).
 #pragma once
 
+#include <cmath>
+#include <vector>
+
 #include "lpr_fft.cuh"
 
 namespace lpr {
@@ -105,12 +108,19 @@ struct Dft<32, INV> {
 template <int S>
 __host__ __device__ constexpr int ct_pad(int i) { return S ? i + (i >> S) : i; }
 
+// Per-pass twiddle tables: pass (R, NS) stores W_{NS R}^{k r}, r = 1..R-1, at
+// OFF + k RS + (r - 1) with RS = R-1 rounded up to even, so a thread's
+// twiddles are contiguous (float4 pairs) and consecutive butterflies read
+// consecutive addresses. (Indexing one length-N table by k r N/(NS R)
+// scatters a warp over up to 32 cache lines per load.)
+__host__ __device__ constexpr int tw_rs(int R) { return (R - 1 + 1) / 2 * 2; }
+
 // One in-place pass of radix R at Stockham stride NS over a padded buffer.
-template <int N, int T, int S, int R, int NS, bool INV>
-__device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw, int tid) {
+template <int N, int T, int S, int R, int NS, int OFF, bool INV>
+__device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ twp, int tid) {
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
-    constexpr int STRIDE = N / (NS * R);
+    constexpr int RS = tw_rs(R);
     float2 v[NB][R];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -127,10 +137,16 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
         if (b < B) {
             const int k = b % NS;
             if (NS > 1) {
+                const float4* w4 = reinterpret_cast<const float4*>(twp + OFF + k * RS);
 #pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    const float2 w = __ldg(tw + k * r * STRIDE);
-                    v[i][r] = INV ? cmulc(v[i][r], w) : cmul(v[i][r], w);
+                for (int r = 1; r < R; r += 2) {
+                    const float4 q = __ldg(w4 + (r - 1) / 2);
+                    const float2 w0 = make_float2(q.x, q.y);
+                    v[i][r] = INV ? cmulc(v[i][r], w0) : cmul(v[i][r], w0);
+                    if (r + 1 < R) {
+                        const float2 w1 = make_float2(q.z, q.w);
+                        v[i][r + 1] = INV ? cmulc(v[i][r + 1], w1) : cmul(v[i][r + 1], w1);
+                    }
                 }
             }
             Dft<R, INV>::run(v[i]);
@@ -142,10 +158,27 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
     __syncthreads();
 }
 
-template <int N, int T, int S, bool INV, int NS, int R, int... Rest>
-__device__ __forceinline__ void ct_run(float2* x, const float2* tw, int tid) {
-    ct_pass<N, T, S, R, NS, INV>(x, tw, tid);
-    if constexpr (sizeof...(Rest) > 0) ct_run<N, T, S, INV, NS * R, Rest...>(x, tw, tid);
+template <int N, int T, int S, bool INV, int NS, int OFF, int R, int... Rest>
+__device__ __forceinline__ void ct_run(float2* x, const float2* twp, int tid) {
+    ct_pass<N, T, S, R, NS, OFF, INV>(x, twp, tid);
+    if constexpr (sizeof...(Rest) > 0)
+        ct_run<N, T, S, INV, NS * R, OFF + (NS > 1 ? NS * tw_rs(R) : 0), Rest...>(x, twp, tid);
+}
+
+// Host side: the per-pass table in exactly the order ct_run consumes it.
+template <int N, int NS, int R, int... Rest>
+void ct_twiddles(std::vector<float2>& out) {
+    if (NS > 1) {
+        const int rs = tw_rs(R);
+        const size_t off = out.size();
+        out.resize(off + size_t(NS) * rs, make_float2(0.f, 0.f));
+        for (int k = 0; k < NS; ++k)
+            for (int r = 1; r < R; ++r) {
+                const double a = -2.0 * 3.14159265358979323846 * double(k) * double(r) / double(NS * R);
+                out[off + size_t(k) * rs + (r - 1)] = make_float2(float(std::cos(a)), float(std::sin(a)));
+            }
+    }
+    if constexpr (sizeof...(Rest) > 0) ct_twiddles<N, NS * R, Rest...>(out);
 }
 
 // FFT policies: idx() (the buffer slot of element i), elems() (shared
@@ -167,8 +200,14 @@ struct CtFft {
     __host__ __device__ static int elems(const FftDesc&) { return kElems; }
     template <bool INV>
     __device__ __forceinline__ static float2* run(float2* x, float2*, const FftDesc& d, int gtid) {
-        ct_run<N, T, S, INV, 1, R...>(x, d.tw, gtid);
+        ct_run<N, T, S, INV, 1, 0, R...>(x, d.twp, gtid);
         return x;
+    }
+    static std::vector<float2> pass_twiddles() {
+        std::vector<float2> t;
+        ct_twiddles<N, 1, R...>(t);
+        if (t.empty()) t.push_back(make_float2(1.f, 0.f));
+        return t;
     }
 };
 

@@ -220,14 +220,31 @@ __device__ __forceinline__ void load_packed_hermitian(float2* const* sm, const f
     }
 }
 
-__device__ __forceinline__ float gather_image(const DevGeom& g, const float* __restrict__ q, float cm, float sm,
-                                              float er, float ct, float st) {
-    const float dx = fmaf(er, ct, -g.one_m_aR), dy = er * st;
-    if (fmaf(dx, dx, dy * dy) > g.aR2) return 0.f;  // outside the sector disc D
-    const float ux = dx * g.inv_aR, uy = dy * g.inv_aR;
-    const float xp = fmaf(cm, ux, -sm * uy), yp = fmaf(sm, ux, cm * uy);  // T_m^{-1}, physical units
-    const float half = 0.5f * g.N;
-    const float tc = fmaf(xp, half, half), tr = fmaf(yp, half, half);
+// Fine-grid point -> image sample coordinates. For fine row theta' (ct, st)
+// and column radius e^rho = er, T_m^{-1}(er (ct, st)) in pixels is affine in
+// er: (tc, tr) = er (uc, ur) + (vc_m, vr_m); the sector-disc test
+// |er e^{i theta'} - (1 - aR)|^2 <= aR^2 is er (er - 2 (1 - aR) ct) + 1 - 2 aR <= 0.
+struct FineRow {
+    float uc, ur, c2;
+};
+
+__device__ __forceinline__ FineRow fine_row(const DevGeom& g, float cm, float sm, float ct, float st) {
+    const float sc = 0.5f * g.N * g.inv_aR;
+    return {sc * fmaf(cm, ct, -sm * st), sc * fmaf(sm, ct, cm * st), 2.f * g.one_m_aR * ct};
+}
+
+__device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, float vc, float vr, float er, float& tc,
+                                         float& tr) {
+    if (fmaf(er, er - r.c2, g.mask_k) > 0.f) return false;  // outside the sector disc D
+    tc = fmaf(er, r.uc, vc);
+    tr = fmaf(er, r.ur, vr);
+    return true;
+}
+
+__device__ __forceinline__ float gather_image(const DevGeom& g, const float* __restrict__ q, const FineRow& r,
+                                              float vc, float vr, float er) {
+    float tc, tr;
+    if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
     const float kc = floorf(tc), kr = floorf(tr);
     float wc[4], wr[4];
     bsw(tc - kc, wc);
@@ -262,19 +279,19 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         sm[F::idx(nf / 2 + Lf / 4 + i)] = make_float2(0.f, 0.f);
     }
     const float* q = qf + size_t(b) * g.pitch * g.pitch;
-    const float cm = g.cosm[m], smm = g.sinm[m];
+    const float cm = g.cosm[m], smm = g.sinm[m], vc = g.vcm[m], vr = g.vrm[m];
     const bool one = l0 < g.n_rho, two = l0 + 1 < g.n_rho;
     const float er0 = one ? __ldg(g.erho + l0) : 0.f;
     const float er1 = two ? __ldg(g.erho + l0 + 1) : 0.f;
     const int half_rows = nf / 2;
     for (int i = G.tid; i < half_rows; i += G.size) {
         const int i2 = i + half_rows;
-        const float ct = __ldg(g.fine_cos + i), st = __ldg(g.fine_sin + i);
-        const float ct2 = __ldg(g.fine_cos + i2), st2 = __ldg(g.fine_sin + i2);
-        const float h0 = one ? gather_image(g, q, cm, smm, er0, ct, st) : 0.f;
-        const float h1 = two ? gather_image(g, q, cm, smm, er1, ct, st) : 0.f;
-        const float h2 = one ? gather_image(g, q, cm, smm, er0, ct2, st2) : 0.f;
-        const float h3 = two ? gather_image(g, q, cm, smm, er1, ct2, st2) : 0.f;
+        const FineRow r1 = fine_row(g, cm, smm, __ldg(g.fine_cos + i), __ldg(g.fine_sin + i));
+        const FineRow r2 = fine_row(g, cm, smm, __ldg(g.fine_cos + i2), __ldg(g.fine_sin + i2));
+        const float h0 = one ? gather_image(g, q, r1, vc, vr, er0) : 0.f;
+        const float h1 = two ? gather_image(g, q, r1, vc, vr, er1) : 0.f;
+        const float h2 = one ? gather_image(g, q, r2, vc, vr, er0) : 0.f;
+        const float h3 = two ? gather_image(g, q, r2, vc, vr, er1) : 0.f;
         sm[F::idx(i - nf / 2 + Lf)] = make_float2(h0, h1);  // q = i - nf/2 < 0
         sm[F::idx(i2 - nf / 2)] = make_float2(h2, h3);      // q = i2 - nf/2 >= 0
     }
@@ -516,21 +533,17 @@ __global__ void LPR_LB(F) k_theta_inv_fine_T(const __grid_constant__ DevGeom g, 
     __syncthreads();
     const float2* res = F::template run<true>(sms[G.g], fft_scratch<F>(sms[G.g], fd), fd, G.tid);
     float* q = qbar + size_t(b) * g.pitch * g.pitch;
-    const float cm = g.cosm[m], smm = g.sinm[m];
-    const float half = 0.5f * g.N;
+    const float cm = g.cosm[m], smm = g.sinm[m], vc = g.vcm[m], vr = g.vrm[m];
     for (int i = G.tid; i < nf; i += G.size) {
         const int qq = i - nf / 2;
         const float2 z = res[F::idx(qq < 0 ? qq + Lf : qq)];
-        const float ct = __ldg(g.fine_cos + i), st = __ldg(g.fine_sin + i);
+        const FineRow rw = fine_row(g, cm, smm, __ldg(g.fine_cos + i), __ldg(g.fine_sin + i));
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             if (l0 + c >= n) break;
             const float er = __ldg(g.erho + l0 + c);
-            const float dx = fmaf(er, ct, -g.one_m_aR), dy = er * st;
-            if (fmaf(dx, dx, dy * dy) > g.aR2) continue;
-            const float ux = dx * g.inv_aR, uy = dy * g.inv_aR;
-            const float xp = fmaf(cm, ux, -smm * uy), yp = fmaf(smm, ux, cm * uy);
-            const float tc = fmaf(xp, half, half), tr = fmaf(yp, half, half);
+            float tc, tr;
+            if (!fine_pos(g, rw, vc, vr, er, tc, tr)) continue;
             const float kc = floorf(tc), kr = floorf(tr);
             float wc[4], wr[4];
             bsw(tc - kc, wc);
@@ -593,6 +606,17 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
 }
 
 // ------------------------------------------------------------- host launchers
+std::vector<float2> fft_pass_twiddles(int variant) {
+    switch (variant) {
+        case kFft2048: return Fft2048::pass_twiddles();
+        case kFft4096: return Fft4096::pass_twiddles();
+        case kFft4374: return Fft4374::pass_twiddles();
+        case kFft8192: return Fft8192::pass_twiddles();
+        case kFft16384: return Fft16384::pass_twiddles();
+        default: return {};
+    }
+}
+
 FftLaunch fft_launch_config(const FftDesc& d) {
     const int gt = GenericFft::threads(d);
     FftLaunch L{kFftGeneric, gt, gt, 1, size_t(GenericFft::elems(d)) * sizeof(float2)};

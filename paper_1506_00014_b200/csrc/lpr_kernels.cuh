@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "lpr_fft.cuh"
 
 namespace lpr {
@@ -23,6 +25,8 @@ struct DevGeom {
     int pitch;   // row pitch of the apron image (N + 2 kApron)
     float aR, inv_aR, one_m_aR, aR2, log_ar, inv_drho, inv_dtheta_p, out_scale;
     float cosm[kMaxSectors], sinm[kMaxSectors];
+    float vcm[kMaxSectors], vrm[kMaxSectors];  // pixel coords of T_m^{-1}(0): (N/2)(1 - (cos, sin)(m beta)(1 - aR)/aR)
+    float mask_k;                               // 1 - 2 aR (sector-disc test)
     // tables (device)
     const float* fine_cos;    // nf entries: cos(q dtheta_lp), q = i - nf/2
     const float* fine_sin;
@@ -44,6 +48,7 @@ struct FftLaunch {
 
 // host-side launchers (lpr_kernels.cu)
 FftLaunch fft_launch_config(const FftDesc& d);
+std::vector<float2> fft_pass_twiddles(int variant);
 cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
                                 size_t rho_mult_bytes);
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
