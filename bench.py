@@ -143,14 +143,23 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of each kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")
-    try:
-        with open(path) as f:
-            return json.load(f)
-    except Exception:
-        return {}
+def ncu_traffic(stage: str, slices: int):
+    """dram__bytes_read + dram__bytes_write of `stage`'s kernel from the latest
+    committed `ncu --set full` capture (profiles/*/ncu_dram_bytes.json, per
+    slice), scaled to one launch of `slices` slices; None if not captured."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_dram_bytes.json")), key=os.path.getmtime)
+    for path in reversed(files):
+        try:
+            with open(path) as f:
+                per = json.load(f)["per_slice_bytes"]
+        except Exception:
+            continue
+        for name, b in per.items():
+            if name == "k_" + stage or name.startswith("k_" + stage + "<"):
+                return b * slices
+    return None
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -312,7 +321,7 @@ def run_ours(args):
     total = sum(s["ms"] for s in stages.values())
     dom_name, dom = max(stages.items(), key=lambda kv: kv[1]["ms"])
     peak, peak_kind = measured_peak()
-    traffic = ncu_traffic().get(dom_name.split(":", 1)[1] + ("@R" if dom_name.startswith("R:") else "@R#"))
+    traffic = ncu_traffic(dom_name.split(":", 1)[1], B)
     for s in stages.values():
         s["share"] = s["ms"] / total
         s["frac"] = s["GBps"] / peak

@@ -109,18 +109,17 @@ template <int S>
 __host__ __device__ constexpr int ct_pad(int i) { return S ? i + (i >> S) : i; }
 
 // Per-pass twiddle tables: pass (R, NS) stores W_{NS R}^{k r}, r = 1..R-1, at
-// OFF + k RS + (r - 1) with RS = R-1 rounded up to even, so a thread's
-// twiddles are contiguous (float4 pairs) and consecutive butterflies read
-// consecutive addresses. (Indexing one length-N table by k r N/(NS R)
-// scatters a warp over up to 32 cache lines per load.)
-__host__ __device__ constexpr int tw_rs(int R) { return (R - 1 + 1) / 2 * 2; }
+// OFF + (r - 1) NS + k, so for each r the butterflies of a warp (consecutive
+// k) read consecutive float2: two fully used wavefronts per load. (Indexing
+// one length-N table by k r N/(NS R) scatters a warp over up to 32 cache
+// lines per load; a [k][r] layout still strides lanes by R float2.)
+__host__ __device__ constexpr int tw_rs(int R) { return R - 1; }
 
 // One in-place pass of radix R at Stockham stride NS over a padded buffer.
 template <int N, int T, int S, int R, int NS, int OFF, bool INV>
 __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ twp, int tid) {
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
-    constexpr int RS = tw_rs(R);
     float2 v[NB][R];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -137,16 +136,10 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
         if (b < B) {
             const int k = b % NS;
             if (NS > 1) {
-                const float4* w4 = reinterpret_cast<const float4*>(twp + OFF + k * RS);
 #pragma unroll
-                for (int r = 1; r < R; r += 2) {
-                    const float4 q = __ldg(w4 + (r - 1) / 2);
-                    const float2 w0 = make_float2(q.x, q.y);
-                    v[i][r] = INV ? cmulc(v[i][r], w0) : cmul(v[i][r], w0);
-                    if (r + 1 < R) {
-                        const float2 w1 = make_float2(q.z, q.w);
-                        v[i][r + 1] = INV ? cmulc(v[i][r + 1], w1) : cmul(v[i][r + 1], w1);
-                    }
+                for (int r = 1; r < R; ++r) {
+                    const float2 w = __ldg(twp + OFF + (r - 1) * NS + k);
+                    v[i][r] = INV ? cmulc(v[i][r], w) : cmul(v[i][r], w);
                 }
             }
             Dft<R, INV>::run(v[i]);
@@ -175,7 +168,7 @@ void ct_twiddles(std::vector<float2>& out) {
         for (int k = 0; k < NS; ++k)
             for (int r = 1; r < R; ++r) {
                 const double a = -2.0 * 3.14159265358979323846 * double(k) * double(r) / double(NS * R);
-                out[off + size_t(k) * rs + (r - 1)] = make_float2(float(std::cos(a)), float(std::sin(a)));
+                out[off + size_t(r - 1) * NS + k] = make_float2(float(std::cos(a)), float(std::sin(a)));
             }
     }
     if constexpr (sizeof...(Rest) > 0) ct_twiddles<N, NS * R, Rest...>(out);

@@ -146,6 +146,22 @@ __device__ __forceinline__ float2* fft_scratch(float2* sm, const FftDesc& d) {
     return sm + (d.nb ? d.nb : d.n);
 }
 
+// The kP transform buffers of a block, addressed arithmetically (an array of
+// pointers indexed by a runtime p would live in local memory).
+struct Slots {
+    float2* base;
+    int stride;
+    __device__ __forceinline__ float2* operator()(int p) const { return base + p * stride; }
+};
+
+// Where the results are: compile-time plans run in place (slot p = smem + p E);
+// the generic plan (kP = 1) may finish in its scratch half.
+template <class F>
+__device__ __forceinline__ Slots result_slots(float2* smem, int E, float2* res) {
+    if constexpr (F::kT > 0) return Slots{smem, E};
+    return Slots{res, 0};
+}
+
 // Pair the block's columns: pair p of the block covers columns l0 + 2p, l0 + 2p + 1.
 __device__ __forceinline__ bool col_ok(int l, int n) { return l < n; }
 
@@ -153,7 +169,7 @@ __device__ __forceinline__ bool col_ok(int l, int n) { return l < n; }
 // for all kP pairs of the block; consecutive threads take consecutive pairs of
 // one row (float4 each when aligned). The theta Nyquist row is zeroed.
 template <class F>
-__device__ __forceinline__ void store_half_spectra(const float2* const* res, int L, int nts, int n_rho, int l0,
+__device__ __forceinline__ void store_half_spectra(Slots res, int L, int nts, int n_rho, int l0,
                                                    float2* __restrict__ out) {
     constexpr int P = F::kP;
     for (int e = threadIdx.x; e < (nts + 1) * P; e += blockDim.x) {
@@ -162,7 +178,7 @@ __device__ __forceinline__ void store_half_spectra(const float2* const* res, int
         if (l >= n_rho) continue;
         float2 A = make_float2(0.f, 0.f), B = A;
         if (k < nts) {
-            const float2 z = res[p][F::idx(k)], zm = res[p][F::idx(k == 0 ? 0 : L - k)];
+            const float2 z = res(p)[F::idx(k)], zm = res(p)[F::idx(k == 0 ? 0 : L - k)];
             A = make_float2(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y));
             B = make_float2(0.5f * (z.y + zm.y), -0.5f * (z.x - zm.x));
         }
@@ -179,16 +195,16 @@ __device__ __forceinline__ void store_half_spectra(const float2* const* res, int
 // Load half spectra rows k in [0, kmax) of the block's pairs and rebuild each
 // packed Hermitian transform of length L: Z(k) = A + iB, Z(L-k) = conj(A) + i conj(B).
 template <class F>
-__device__ __forceinline__ void put_packed(float2* const* sm, int k, int p, int L, float2 A, float2 B) {
-    sm[p][F::idx(k)] = make_float2(A.x - B.y, A.y + B.x);
-    if (k > 0) sm[p][F::idx(L - k)] = make_float2(A.x + B.y, B.x - A.y);
+__device__ __forceinline__ void put_packed(Slots sm, int k, int p, int L, float2 A, float2 B) {
+    sm(p)[F::idx(k)] = make_float2(A.x - B.y, A.y + B.x);
+    if (k > 0) sm(p)[F::idx(L - k)] = make_float2(A.x + B.y, B.x - A.y);
 }
 
 template <class F>
-__device__ __forceinline__ void load_packed_hermitian(float2* const* sm, const float2* __restrict__ in, int kmax,
+__device__ __forceinline__ void load_packed_hermitian(Slots sm, const float2* __restrict__ in, int kmax,
                                                       int L, int n, int l0) {
     constexpr int P = F::kP;
-    constexpr int U = 8;  // independent 16-byte loads in flight per thread
+    constexpr int U = 4;  // independent 16-byte loads in flight per thread
     const int total = kmax * P;
     const bool vec = l0 + 2 * P <= n && (n % 2) == 0 && (reinterpret_cast<uintptr_t>(in + l0) & 15) == 0;
     if (vec) {
@@ -296,13 +312,9 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         sm[F::idx(i2 - nf / 2)] = make_float2(h2, h3);      // q = i2 - nf/2 >= 0
     }
     __syncthreads();
-    float2* res[F::kP];
-    res[G.g] = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
-    __shared__ float2* rptr[F::kP];
-    if (G.tid == 0) rptr[G.g] = res[G.g];
-    __syncthreads();
+    float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
     float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
-    store_half_spectra<F>(rptr, Lf, g.nts, g.n_rho, l0b, out);
+    store_half_spectra<F>(result_slots<F>(smem, E, res), Lf, g.nts, g.n_rho, l0b, out);
 }
 
 // rho pass: for every (item, k_theta) row, FFT along rho, multiply by the
@@ -344,26 +356,22 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
     constexpr int P = F::kP;
     const Group<F> G;
     const int E = F::elems(fd);
-    float2* sms[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) sms[p] = smem + p * E;
+    const Slots sms{smem, E};
     const int m = blockIdx.y, b = blockIdx.z;
     const int l0b = 2 * P * blockIdx.x;
     const int nts = g.nts, L2 = g.L2, n = g.n_rho;
     const size_t item = size_t(b) * g.M + m;
-    if (threadIdx.x < P) sms[threadIdx.x][F::idx(nts)] = make_float2(0.f, 0.f);  // zeroed band edge
+    if (threadIdx.x < P) sms(threadIdx.x)[F::idx(nts)] = make_float2(0.f, 0.f);  // zeroed band edge
     load_packed_hermitian<F>(sms, spec + item * size_t(nts + 1) * n, nts, L2, n, l0b);
     __syncthreads();
-    float2* res = F::template run<true>(sms[G.g], fft_scratch<F>(sms[G.g], fd), fd, G.tid);
-    __shared__ float2* rptr[P];
-    if (G.tid == 0) rptr[G.g] = res;
-    __syncthreads();
+    float2* res = F::template run<true>(sms(G.g), fft_scratch<F>(sms(G.g), fd), fd, G.tid);
+    const Slots rs = result_slots<F>(smem, E, res);
     float* out = lp + item * size_t(g.win) * n;
     for (int e = threadIdx.x; e < g.win * P; e += blockDim.x) {
         const int r = e / P, p = e % P;
         const int l = l0b + 2 * p;
         if (l >= n) continue;
-        const float2 z = rptr[p][F::idx(wrapi(g.j0 + r, L2))];
+        const float2 z = rs(p)[F::idx(wrapi(g.j0 + r, L2))];
         float* dst = out + size_t(r) * n + l;
         if (l + 1 < n && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
             *reinterpret_cast<float2*>(dst) = z;
@@ -469,11 +477,8 @@ __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, cons
     }
     __syncthreads();
     float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
-    __shared__ float2* rptr[F::kP];
-    if (G.tid == 0) rptr[G.g] = res;
-    __syncthreads();
     float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * g.n_rho;
-    store_half_spectra<F>(rptr, L2, nts, g.n_rho, l0b, out);
+    store_half_spectra<F>(result_slots<F>(smem, E, res), L2, nts, g.n_rho, l0b, out);
 }
 
 // R^T stage 2: real theta FFT of the lattice rows [-nts/2, nts/2) held in
@@ -504,11 +509,8 @@ __global__ void LPR_LB(F) k_theta_fwd_T(const __grid_constant__ DevGeom g, const
     __syncthreads();
     float2* sm = smem + G.g * E;
     float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
-    __shared__ float2* rptr[P];
-    if (G.tid == 0) rptr[G.g] = res;
-    __syncthreads();
     float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * n;
-    store_half_spectra<F>(rptr, L2, nts, n, l0b, out);
+    store_half_spectra<F>(result_slots<F>(smem, E, res), L2, nts, n, l0b, out);
 }
 
 // R^T stage 4: Hermitian inverse over the doubled fine period (zero beyond
@@ -521,17 +523,15 @@ __global__ void LPR_LB(F) k_theta_inv_fine_T(const __grid_constant__ DevGeom g, 
     constexpr int P = F::kP;
     const Group<F> G;
     const int E = F::elems(fd);
-    float2* sms[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) sms[p] = smem + p * E;
+    const Slots sms{smem, E};
     const int m = blockIdx.y, b = blockIdx.z;
     const int l0b = 2 * P * blockIdx.x, l0 = l0b + 2 * G.g;
     const int nts = g.nts, Lf = g.Lf, n = g.n_rho, nf = g.nf;
     const size_t item = size_t(b) * g.M + m;
-    for (int k = nts + G.tid; k <= Lf - nts; k += G.size) sms[G.g][F::idx(k)] = make_float2(0.f, 0.f);
+    for (int k = nts + G.tid; k <= Lf - nts; k += G.size) sms(G.g)[F::idx(k)] = make_float2(0.f, 0.f);
     load_packed_hermitian<F>(sms, spec + item * size_t(nts + 1) * n, nts, Lf, n, l0b);
     __syncthreads();
-    const float2* res = F::template run<true>(sms[G.g], fft_scratch<F>(sms[G.g], fd), fd, G.tid);
+    const float2* res = F::template run<true>(sms(G.g), fft_scratch<F>(sms(G.g), fd), fd, G.tid);
     float* q = qbar + size_t(b) * g.pitch * g.pitch;
     const float cm = g.cosm[m], smm = g.sinm[m], vc = g.vcm[m], vr = g.vrm[m];
     for (int i = G.tid; i < nf; i += G.size) {
