@@ -18,7 +18,7 @@
 namespace lpr {
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
-__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* img, float* qf);
+__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* img, float4* q4);
 __global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* sino, float* qg);
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
 __global__ void k_bp_out(DevGeom g, const float* lp, float* img);
@@ -119,6 +119,7 @@ struct lpr_gpu_plan {
     float* band = nullptr;       // banded transpose of the apron-extended 1-D prefilter
     int band_h = 0;
     float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
+    float4* q4 = nullptr;  // quad-tap coefficient raster (R); qf aliases it as the R^T scatter target
     float2* spec = nullptr;
     float *d_in = nullptr, *d_out = nullptr;   // staging for the *_host entry points
     float *h_in = nullptr, *h_out = nullptr;   // pinned
@@ -323,7 +324,8 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
 
     const size_t B = size_t(p->max_batch);
     p->tmp = p->dalloc<float>(B * G.N * g.pitch);
-    p->qf = p->dalloc<float>(B * g.pitch * g.pitch);
+    p->q4 = p->dalloc<float4>(B * g.pitch * g.pitch);
+    p->qf = reinterpret_cast<float*>(p->q4);
     p->qg = p->dalloc<float>(B * G.n_theta * G.N);
     p->spec = p->dalloc<float2>(B * G.M * (nts + 1) * nr);
     p->lp = p->dalloc<float>(B * G.M * g.win * nr);
@@ -350,9 +352,9 @@ inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
 void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
     mark(p, 0, st);
-    k_prefilter_2d<<<dim3(cdiv(g.pitch, 32), cdiv(g.pitch, 32), nb), 256, 0, st>>>(g, img, p->qf);
+    k_prefilter_2d<<<dim3(cdiv(g.pitch, 32), cdiv(g.pitch, 32), nb), 256, 0, st>>>(g, img, p->q4);
     mark(p, 1, st);
-    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->qf, p->spec);
+    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->q4, p->spec);
     mark(p, 2, st);
     launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_R, p->spec);
     mark(p, 3, st);

@@ -60,40 +60,51 @@ __device__ __forceinline__ void bsw(float a, float w[4]) {
 // a (32 + 32)^2 input tile is staged in shared memory through the mirror
 // map, filtered along rows, then along columns (reference order: rows then
 // columns, bspline.cpp:120-129).
-constexpr int kPT = 32;                  // output tile edge
-constexpr int kPE = kPT + 2 * kFirHalf;  // staged input edge
+constexpr int kPT = 32;                      // output tile edge (rows; quad origins per row)
+constexpr int kPX = kPT + 3;                 // coefficient columns per tile row (quad = 4 taps)
+constexpr int kPEY = kPT + 2 * kFirHalf;     // staged input rows
+constexpr int kPEX = kPX + 2 * kFirHalf;     // staged input columns
 
-__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* __restrict__ img, float* __restrict__ qf) {
+// Output: the quad-tap raster q4[r][c] = (Q[r][c], Q[r][c+1], Q[r][c+2], Q[r][c+3])
+// over the apron-extended grid, so every spline tap row of the fine-grid
+// gather is one 16-byte load (4 loads per sample instead of 16).
+__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* __restrict__ img, float4* __restrict__ q4) {
     __shared__ float h[2 * kFirHalf + 1];
-    __shared__ float in[kPE][kPE + 1];
-    __shared__ float mid[kPE][kPT + 1];
+    __shared__ float in[kPEY][kPEX + 1];
+    __shared__ float mid[kPEY][kPX + 1];
+    __shared__ float fin[kPT][kPX + 1];
     const int tid = threadIdx.x;
     const int N = g.N, pitch = g.pitch;
     const int x0 = blockIdx.x * kPT, y0 = blockIdx.y * kPT, b = blockIdx.z;
     if (tid < 2 * kFirHalf + 1) h[tid] = __ldg(g.fir + tid);
     const float* src = img + size_t(b) * N * N;
     const int vx0 = x0 - kApron - kFirHalf, vy0 = y0 - kApron - kFirHalf;
-    for (int i = tid / kPE; i < kPE; i += 256 / kPE) {
-        const float* row = src + size_t(mirror_idx(vy0 + i, N)) * N;
-        const int j = tid % kPE;
-        in[i][j] = __ldg(row + mirror_idx(vx0 + j, N));
+    for (int idx = tid; idx < kPEY * kPEX; idx += 256) {
+        const int i = idx / kPEX, j = idx % kPEX;
+        in[i][j] = __ldg(src + size_t(mirror_idx(vy0 + i, N)) * N + mirror_idx(vx0 + j, N));
     }
     __syncthreads();
-    for (int idx = tid; idx < kPE * kPT; idx += 256) {
-        const int i = idx / kPT, j = idx % kPT;
+    for (int idx = tid; idx < kPEY * kPX; idx += 256) {
+        const int i = idx / kPX, j = idx % kPX;
         float acc = 0.f;
 #pragma unroll
         for (int d = 0; d <= 2 * kFirHalf; ++d) acc = fmaf(h[d], in[i][j + d], acc);
         mid[i][j] = acc;
     }
     __syncthreads();
-    float* dst = qf + size_t(b) * pitch * pitch;
-    for (int idx = tid; idx < kPT * kPT; idx += 256) {
-        const int i = idx / kPT, j = idx % kPT;
+    for (int idx = tid; idx < kPT * kPX; idx += 256) {
+        const int i = idx / kPX, j = idx % kPX;
         float acc = 0.f;
 #pragma unroll
         for (int d = 0; d <= 2 * kFirHalf; ++d) acc = fmaf(h[d], mid[i + d][j], acc);
-        if (y0 + i < pitch && x0 + j < pitch) dst[size_t(y0 + i) * pitch + x0 + j] = acc;
+        fin[i][j] = acc;
+    }
+    __syncthreads();
+    float4* dst = q4 + size_t(b) * pitch * pitch;
+    for (int idx = tid; idx < kPT * kPT; idx += 256) {
+        const int i = idx / kPT, j = idx % kPT;
+        if (y0 + i < pitch && x0 + j < pitch)
+            dst[size_t(y0 + i) * pitch + x0 + j] = make_float4(fin[i][j], fin[i][j + 1], fin[i][j + 2], fin[i][j + 3]);
     }
 }
 
@@ -257,7 +268,7 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
     return true;
 }
 
-__device__ __forceinline__ float gather_image(const DevGeom& g, const float* __restrict__ q, const FineRow& r,
+__device__ __forceinline__ float gather_image(const DevGeom& g, const float4* __restrict__ q4, const FineRow& r,
                                               float vc, float vr, float er) {
     float tc, tr;
     if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
@@ -265,13 +276,12 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const float* __r
     float wc[4], wr[4];
     bsw(tc - kc, wc);
     bsw(tr - kr, wr);
-    const float* p = q + (int(kr) - 1 + kApron) * g.pitch + (int(kc) - 1 + kApron);
+    const float4* p = q4 + (int(kr) - 1 + kApron) * g.pitch + (int(kc) - 1 + kApron);
     float acc = 0.f;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const float* row = p + a * g.pitch;
-        const float v = fmaf(wc[0], __ldg(row), fmaf(wc[1], __ldg(row + 1), fmaf(wc[2], __ldg(row + 2), wc[3] * __ldg(row + 3))));
-        acc = fmaf(wr[a], v, acc);
+        const float4 t = __ldg(p + a * g.pitch);
+        acc = fmaf(wr[a], fmaf(wc[0], t.x, fmaf(wc[1], t.y, fmaf(wc[2], t.z, wc[3] * t.w))), acc);
     }
     return er * acc;
 }
@@ -282,7 +292,7 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const float* __r
 // in flight) to hide the L2 latency of the spline taps.
 template <class F>
 __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                            const float* __restrict__ qf, float2* __restrict__ spec) {
+                                            const float4* __restrict__ qf, float2* __restrict__ spec) {
     extern __shared__ float2 smem[];
     const Group<F> G;
     const int E = F::elems(fd);
@@ -294,7 +304,7 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         sm[F::idx(nf / 2 + i)] = make_float2(0.f, 0.f);
         sm[F::idx(nf / 2 + Lf / 4 + i)] = make_float2(0.f, 0.f);
     }
-    const float* q = qf + size_t(b) * g.pitch * g.pitch;
+    const float4* q = qf + size_t(b) * g.pitch * g.pitch;
     const float cm = g.cosm[m], smm = g.sinm[m], vc = g.vcm[m], vr = g.vrm[m];
     const bool one = l0 < g.n_rho, two = l0 + 1 < g.n_rho;
     const float er0 = one ? __ldg(g.erho + l0) : 0.f;
@@ -678,7 +688,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 }
 
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const float* qf, float2* spec) {
+                            const float4* qf, float2* spec) {
 #define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL

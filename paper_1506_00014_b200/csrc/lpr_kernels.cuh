@@ -52,7 +52,7 @@ std::vector<float2> fft_pass_twiddles(int variant);
 cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
                                 size_t rho_mult_bytes);
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const float* qf, float2* spec);
+                            const float4* qf, float2* spec);
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec);
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
