@@ -8,7 +8,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblpradon_gpu.so")
+LIB_PATH = os.environ.get("LPR_GPU_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                         "liblpradon_gpu.so")
 
 LPR_OK, LPR_ERR_ARG, LPR_ERR_CUDA, LPR_ERR_OOM = 0, 1, 2, 3
 

@@ -14,8 +14,13 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "liblpradon_gpu.so")
+# Experiment variants: LPR_VARIANT=name builds liblpradon_gpu_<name>.so with
+# the extra nvcc defines in LPR_DEFS (e.g. "-DLPR_TAPS=1"); the default build
+# is the product library.
+_VARIANT = os.environ.get("LPR_VARIANT", "")
+BUILD = os.path.join(PKG, "_build" + (f"_{_VARIANT}" if _VARIANT else ""))
+LIB = os.path.join(PKG, "liblpradon_gpu" + (f"_{_VARIANT}" if _VARIANT else "") + ".so")
+EXTRA_DEFS = os.environ.get("LPR_DEFS", "").split() if _VARIANT else []
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
@@ -66,7 +71,7 @@ def build(verbose: bool = False) -> str:
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
         if _stale(o, [s] + headers):
-            jobs.append(([nvcc, "-ccbin", _host_cxx(), *ARCH, *NVCC_FLAGS, "-c", s, "-o", o], o + ".log"))
+            jobs.append(([nvcc, "-ccbin", _host_cxx(), *ARCH, *NVCC_FLAGS, *EXTRA_DEFS, "-c", s, "-o", o], o + ".log"))
     for src in CXX_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")

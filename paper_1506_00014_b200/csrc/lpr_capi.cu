@@ -18,7 +18,7 @@
 namespace lpr {
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
-__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* img, float4* q4);
+__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* img, Tap* q4);
 __global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* sino, float* qg);
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
 __global__ void k_bp_out(DevGeom g, const float* lp, float* img);
@@ -119,11 +119,13 @@ struct lpr_gpu_plan {
     float* band = nullptr;       // banded transpose of the apron-extended 1-D prefilter
     int band_h = 0;
     float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
-    float4* q4 = nullptr;  // quad-tap coefficient raster (R); qf aliases it as the R^T scatter target
+    Tap* q4 = nullptr;  // coefficient raster read by the R gather; qf aliases it as the R^T scatter target
     float2* spec = nullptr;
     float *d_in = nullptr, *d_out = nullptr;   // staging for the *_host entry points
     float *h_in = nullptr, *h_out = nullptr;   // pinned
     cudaStream_t stream = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     std::vector<void*> allocs;
     long long launches = 0, ffts = 0;
@@ -191,6 +193,13 @@ struct lpr_gpu_plan {
         for (void* p : allocs) cudaFree(p);
         if (h_in) cudaFreeHost(h_in);
         if (h_out) cudaFreeHost(h_out);
+        for (int i = 0; i < 2; ++i) {
+            if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
+            if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
+            if (ev_d2h[i]) cudaEventDestroy(ev_d2h[i]);
+        }
+        if (s_in) cudaStreamDestroy(s_in);
+        if (s_out) cudaStreamDestroy(s_out);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -324,7 +333,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
 
     const size_t B = size_t(p->max_batch);
     p->tmp = p->dalloc<float>(B * G.N * g.pitch);
-    p->q4 = p->dalloc<float4>(B * g.pitch * g.pitch);
+    p->q4 = p->dalloc<Tap>(B * g.pitch * g.pitch);
     p->qf = reinterpret_cast<float*>(p->q4);
     p->qg = p->dalloc<float>(B * G.n_theta * G.N);
     p->spec = p->dalloc<float2>(B * G.M * (nts + 1) * nr);
@@ -335,6 +344,13 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     ck(cudaHostAlloc(&p->h_in, io * sizeof(float), cudaHostAllocDefault), "cudaHostAlloc");
     ck(cudaHostAlloc(&p->h_out, io * sizeof(float), cudaHostAllocDefault), "cudaHostAlloc");
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 2; ++i) {
+        ck(cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&p->ev_d2h[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
 
     ck(prepare_fft_kernels(p->l_fine, p->l_rho, p->l_coarse, size_t(G.n_rho) * sizeof(float2)),
        "fft smem attributes");
@@ -425,12 +441,41 @@ bool is_pinned(const void* ptr) {
     return a.type == cudaMemoryTypeHost;
 }
 
+// Host-buffer path. With pinned user buffers the batch is cut into chunks
+// that flow through a three-stream pipeline (H2D of chunk i+1 and D2H of
+// chunk i-1 overlap the compute of chunk i; two device slots, events order
+// slot reuse). Pageable buffers are staged through the plan's pinned buffers
+// one chunk at a time.
 void run_host(lpr_gpu_plan* p, ChunkFn fn, const float* hin, float* hout, int batch, size_t in_sz, size_t out_sz) {
     if (!p) throw std::invalid_argument("null plan");
     if (batch < 0 || (batch > 0 && (!hin || !hout))) throw std::invalid_argument("bad buffers or batch");
     ck(cudaSetDevice(p->device), "cudaSetDevice");
     const bool pin_in = is_pinned(hin), pin_out = is_pinned(hout);
     cudaStream_t st = p->stream;
+    if (pin_in && pin_out && batch > 1 && p->max_batch > 1) {
+        const int c = std::max(1, std::min(p->max_batch / 2, (batch + 3) / 4));
+        const int chunks = (batch + c - 1) / c;
+        for (int i = 0; i < chunks; ++i) {
+            const int slot = i & 1, b0 = i * c, nb = std::min(c, batch - b0);
+            float* din = p->d_in + size_t(slot) * c * in_sz;
+            float* dout = p->d_out + size_t(slot) * c * out_sz;
+            if (i >= 2) ck(cudaStreamWaitEvent(p->s_in, p->ev_comp[slot], 0), "wait");
+            ck(cudaMemcpyAsync(din, hin + size_t(b0) * in_sz, size_t(nb) * in_sz * sizeof(float),
+                               cudaMemcpyHostToDevice, p->s_in), "H2D");
+            ck(cudaEventRecord(p->ev_h2d[slot], p->s_in), "event");
+            ck(cudaStreamWaitEvent(st, p->ev_h2d[slot], 0), "wait");
+            if (i >= 2) ck(cudaStreamWaitEvent(st, p->ev_d2h[slot], 0), "wait");
+            fn(p, din, dout, nb, st);
+            ck(cudaEventRecord(p->ev_comp[slot], st), "event");
+            ck(cudaStreamWaitEvent(p->s_out, p->ev_comp[slot], 0), "wait");
+            ck(cudaMemcpyAsync(hout + size_t(b0) * out_sz, dout, size_t(nb) * out_sz * sizeof(float),
+                               cudaMemcpyDeviceToHost, p->s_out), "D2H");
+            ck(cudaEventRecord(p->ev_d2h[slot], p->s_out), "event");
+        }
+        ck(cudaStreamSynchronize(p->s_out), "stream sync");
+        ck(cudaStreamSynchronize(st), "stream sync");
+        return;
+    }
     for (int b0 = 0; b0 < batch; b0 += p->max_batch) {
         const int nb = std::min(p->max_batch, batch - b0);
         const float* src = hin + size_t(b0) * in_sz;

@@ -227,7 +227,7 @@ struct GenericFft {
 using Fft2048 = CtFft<2048, 128, 4, 2, 4, 16, 16, 8>;
 using Fft4096 = CtFft<4096, 256, 2, 1, 4, 16, 16, 16>;
 using Fft4374 = CtFft<4374, 192, 1, 2, 0, 27, 27, 6>;
-using Fft8192 = CtFft<8192, 256, 1, 2, 5, 32, 16, 16>;
+using Fft8192 = CtFft<8192, 512, 1, 2, 4, 16, 16, 16, 2>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 
 }  // namespace lpr

@@ -68,7 +68,7 @@ constexpr int kPEX = kPX + 2 * kFirHalf;     // staged input columns
 // Output: the quad-tap raster q4[r][c] = (Q[r][c], Q[r][c+1], Q[r][c+2], Q[r][c+3])
 // over the apron-extended grid, so every spline tap row of the fine-grid
 // gather is one 16-byte load (4 loads per sample instead of 16).
-__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* __restrict__ img, float4* __restrict__ q4) {
+__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* __restrict__ img, Tap* __restrict__ q4) {
     __shared__ float h[2 * kFirHalf + 1];
     __shared__ float in[kPEY][kPEX + 1];
     __shared__ float mid[kPEY][kPX + 1];
@@ -100,11 +100,16 @@ __global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* __
         fin[i][j] = acc;
     }
     __syncthreads();
-    float4* dst = q4 + size_t(b) * pitch * pitch;
+    Tap* dst = q4 + size_t(b) * pitch * pitch;
     for (int idx = tid; idx < kPT * kPT; idx += 256) {
         const int i = idx / kPT, j = idx % kPT;
-        if (y0 + i < pitch && x0 + j < pitch)
+        if (y0 + i < pitch && x0 + j < pitch) {
+#if LPR_TAPS == 4
             dst[size_t(y0 + i) * pitch + x0 + j] = make_float4(fin[i][j], fin[i][j + 1], fin[i][j + 2], fin[i][j + 3]);
+#else
+            dst[size_t(y0 + i) * pitch + x0 + j] = fin[i][j];
+#endif
+        }
     }
 }
 
@@ -268,7 +273,7 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
     return true;
 }
 
-__device__ __forceinline__ float gather_image(const DevGeom& g, const float4* __restrict__ q4, const FineRow& r,
+__device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __restrict__ q4, const FineRow& r,
                                               float vc, float vr, float er) {
     float tc, tr;
     if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
@@ -276,11 +281,16 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const float4* __
     float wc[4], wr[4];
     bsw(tc - kc, wc);
     bsw(tr - kr, wr);
-    const float4* p = q4 + (int(kr) - 1 + kApron) * g.pitch + (int(kc) - 1 + kApron);
+    const Tap* p = q4 + (int(kr) - 1 + kApron) * g.pitch + (int(kc) - 1 + kApron);
     float acc = 0.f;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
+#if LPR_TAPS == 4
         const float4 t = __ldg(p + a * g.pitch);
+#else
+        const float* q1 = p + a * g.pitch;
+        const float4 t = make_float4(__ldg(q1), __ldg(q1 + 1), __ldg(q1 + 2), __ldg(q1 + 3));
+#endif
         acc = fmaf(wr[a], fmaf(wc[0], t.x, fmaf(wc[1], t.y, fmaf(wc[2], t.z, wc[3] * t.w))), acc);
     }
     return er * acc;
@@ -292,7 +302,7 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const float4* __
 // in flight) to hide the L2 latency of the spline taps.
 template <class F>
 __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                            const float4* __restrict__ qf, float2* __restrict__ spec) {
+                                            const Tap* __restrict__ qf, float2* __restrict__ spec) {
     extern __shared__ float2 smem[];
     const Group<F> G;
     const int E = F::elems(fd);
@@ -304,7 +314,7 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         sm[F::idx(nf / 2 + i)] = make_float2(0.f, 0.f);
         sm[F::idx(nf / 2 + Lf / 4 + i)] = make_float2(0.f, 0.f);
     }
-    const float4* q = qf + size_t(b) * g.pitch * g.pitch;
+    const Tap* q = qf + size_t(b) * g.pitch * g.pitch;
     const float cm = g.cosm[m], smm = g.sinm[m], vc = g.vcm[m], vr = g.vrm[m];
     const bool one = l0 < g.n_rho, two = l0 + 1 < g.n_rho;
     const float er0 = one ? __ldg(g.erho + l0) : 0.f;
@@ -688,7 +698,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 }
 
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const float4* qf, float2* spec) {
+                            const Tap* qf, float2* spec) {
 #define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL

@@ -11,6 +11,18 @@
 namespace lpr {
 
 constexpr int kMaxSectors = 16;
+
+// Layout of the image B-spline coefficients read by the fine-grid gather:
+// LPR_TAPS 4 = quad-tap float4 rows (4 consecutive coefficients per element,
+// one 16-byte load per tap row), 1 = plain fp32 raster (4 loads per tap row).
+#ifndef LPR_TAPS
+#define LPR_TAPS 4
+#endif
+#if LPR_TAPS == 4
+using Tap = float4;
+#else
+using Tap = float;
+#endif
 constexpr int kApron = 4;     // mirrored border around the image coefficients
 constexpr int kFirHalf = 16;  // B-spline prefilter impulse-response half length
 
@@ -52,7 +64,7 @@ std::vector<float2> fft_pass_twiddles(int variant);
 cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
                                 size_t rho_mult_bytes);
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const float4* qf, float2* spec);
+                            const Tap* qf, float2* spec);
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec);
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,

@@ -110,6 +110,19 @@ def _is_torch(x) -> bool:
 
 
 def _run(plan: RadonPlan, x, in_shape, out_shape, dev_fn, host_fn):
+    if _is_torch(x) and not x.is_cuda:
+        # host tensor (pinned ones take the pipelined H2D/compute/D2H path)
+        import torch
+
+        if x.dtype != torch.float32:
+            raise ValueError("expected a float32 tensor")
+        single = x.dim() == 2
+        xb = (x.unsqueeze(0) if single else x).contiguous()
+        if tuple(xb.shape[1:]) != in_shape:
+            raise ValueError(f"input shape {tuple(x.shape)} does not match the plan {in_shape}")
+        out = torch.empty((xb.shape[0],) + out_shape, dtype=torch.float32, pin_memory=x.is_pinned())
+        check(host_fn(plan.handle, xb.data_ptr(), out.data_ptr(), xb.shape[0]))
+        return out[0] if single else out
     if _is_torch(x):
         import torch
 

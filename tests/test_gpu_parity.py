@@ -86,6 +86,15 @@ def test_host_entry_points_match_device(lp, lpo, cuda):
     devb = lp.fast_backprojection(torch.tensor(dev, device=cuda), plan).cpu().numpy()
     hostb = lp.fast_backprojection(host, plan)
     np.testing.assert_array_equal(devb, hostb)
+    # pinned host tensors take the chunked three-stream pipeline
+    plan4 = lp.RadonPlan(g, z, zb, max_batch=4)
+    f7 = np.concatenate([f, f, f[:1]]).astype(np.float32)  # 7 slices -> chunks of 2, ragged tail
+    pinned = torch.tensor(f7).pin_memory()
+    piped = lp.fast_radon(pinned, plan4)
+    assert piped.is_pinned()
+    np.testing.assert_array_equal(piped.numpy(), lp.fast_radon(torch.tensor(f7, device=cuda), plan4).cpu().numpy())
+    pipedb = lp.fast_backprojection(piped, plan4)
+    np.testing.assert_array_equal(pipedb.numpy(), lp.fast_backprojection(piped.to(cuda), plan4).cpu().numpy())
 
 
 def test_zero_linearity_and_edge_cases(lp, lpo, cuda):
