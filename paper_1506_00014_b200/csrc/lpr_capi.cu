@@ -19,6 +19,8 @@ namespace lpr {
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
 __global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* img, Tap* q4);
+__global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float* img, Tap* q4);
+__global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const float* sino, float* qg);
 __global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* sino, float* qg);
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
 __global__ void k_bp_out(DevGeom g, const float* lp, float* img);
@@ -368,7 +370,7 @@ inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
 void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
     mark(p, 0, st);
-    k_prefilter_2d<<<dim3(cdiv(g.pitch, 32), cdiv(g.pitch, 32), nb), 256, 0, st>>>(g, img, p->q4);
+    k_prefilter_2d_iir<<<dim3(cdiv(g.pitch, 64), cdiv(g.pitch, 64), nb), 128, 0, st>>>(g, img, p->q4);
     mark(p, 1, st);
     launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->q4, p->spec);
     mark(p, 2, st);
@@ -387,7 +389,7 @@ const char* const kRadonStages[] = {"prefilter_2d", "radon_theta_fwd", "rho_pass
 void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
     mark(p, 0, st);
-    k_prefilter_sino<<<dim3(cdiv(g.N, 256), g.n_theta, nb), 256, 0, st>>>(g, sino, p->qg);
+    k_prefilter_sino_iir<<<dim3(cdiv(g.N, 256), cdiv(g.n_theta, 32), nb), 128, 0, st>>>(g, sino, p->qg);
     mark(p, 1, st);
     launch_bp_theta_fwd(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->qg, p->spec);
     mark(p, 2, st);
