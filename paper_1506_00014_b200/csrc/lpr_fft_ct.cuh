@@ -174,6 +174,15 @@ void ct_twiddles(std::vector<float2>& out) {
     if constexpr (sizeof...(Rest) > 0) ct_twiddles<N, NS * R, Rest...>(out);
 }
 
+template <int R1, int... Rest>
+struct RadixPack {
+    static constexpr int first = R1;
+    template <int N, int T, int S, bool INV>
+    __device__ __forceinline__ static void tail(float2* x, const float2* twp, int tid) {
+        if constexpr (sizeof...(Rest) > 0) ct_run<N, T, S, INV, R1, 0, Rest...>(x, twp, tid);
+    }
+};
+
 // FFT policies: idx() (the buffer slot of element i), elems() (shared
 // float2 slots one transform needs), kT threads per transform and kP
 // transforms per block (the theta kernels give each transform two real
@@ -195,6 +204,13 @@ struct CtFft {
     __device__ __forceinline__ static float2* run(float2* x, float2*, const FftDesc& d, int gtid) {
         ct_run<N, T, S, INV, 1, 0, R...>(x, d.twp, gtid);
         return x;
+    }
+    // first radix, and the remaining passes for kernels that run the first
+    // (twiddle-free, NS = 1) pass themselves straight from gathered registers
+    static constexpr int kR1 = RadixPack<R...>::first;
+    template <bool INV>
+    __device__ __forceinline__ static void run_tail(float2* x, const FftDesc& d, int gtid) {
+        RadixPack<R...>::template tail<N, T, S, INV>(x, d.twp, gtid);
     }
     static std::vector<float2> pass_twiddles() {
         std::vector<float2> t;

@@ -391,6 +391,44 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __res
     return er * acc;
 }
 
+// First FFT pass fused with the sample gather, for a real-pair transform of
+// length N whose input occupies rows [0, N/2) placed at positions
+// p = row + N/4 - ... i.e. [0, N/4) <- rows [N/4, N/2) and [3N/4, N) <- rows
+// [0, N/4) (the zero-embedded period), zero elsewhere. Each thread gathers the
+// R1 inputs of its first-pass butterflies into registers (the zero half is
+// skipped at compile time), does the radix-R1 DFT and writes the pass output:
+// no zero fill, no staging store, no first-pass shared read.
+template <class F, class Gather>
+__device__ __forceinline__ void first_pass_gathered(float2* sm, int tid, Gather&& gather) {
+    constexpr int N = F::kN, R1 = F::kR1, B1 = N / R1, T = F::kT;
+    static_assert(R1 % 4 == 0, "first radix must split the zero half");
+    constexpr int NB1 = (B1 + T - 1) / T;
+#pragma unroll
+    for (int i = 0; i < NB1; ++i) {
+        const int bb = tid + i * T;
+        if (bb < B1) {
+            float2 v[R1];
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                if (r < R1 / 4) {
+                    v[r] = gather(bb + B1 * r + N / 4);  // p in [0, N/4)
+                } else if (r >= 3 * R1 / 4) {
+                    v[r] = gather(bb + B1 * r - 3 * N / 4);  // p in [3N/4, N)
+                } else {
+                    v[r] = make_float2(0.f, 0.f);
+                }
+            }
+            Dft<R1, false>::run(v);
+#pragma unroll
+            for (int r = 0; r < R1; ++r) sm[F::idx(bb * R1 + r)] = v[r];
+        }
+    }
+    __syncthreads();
+}
+
+template <class F>
+constexpr bool kFusedFirstPass = F::kT > 0 && (F::kN % 4 == 0);
+
 // Alg. 1 steps 3-6a: gather T_m f e^rho on the fine grid of two rho columns,
 // zero-embed into the doubled fine period Lf, real theta FFT, keep |k| < nts.
 // Each thread gathers two fine rows per iteration (64 independent tap loads
@@ -405,15 +443,28 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
     const int m = blockIdx.y, b = blockIdx.z;
     const int l0b = 2 * F::kP * blockIdx.x, l0 = l0b + 2 * G.g;
     const int Lf = g.Lf, nf = g.nf;
-    for (int i = G.tid; i < Lf / 4; i += G.size) {  // the zero half [nf/2, Lf - nf/2)
-        sm[F::idx(nf / 2 + i)] = make_float2(0.f, 0.f);
-        sm[F::idx(nf / 2 + Lf / 4 + i)] = make_float2(0.f, 0.f);
-    }
     const Tap* q = qf + size_t(b) * g.pitch * g.pitch;
     const float cm = g.cosm[m], smm = g.sinm[m], vc = g.vcm[m], vr = g.vrm[m];
     const bool one = l0 < g.n_rho, two = l0 + 1 < g.n_rho;
     const float er0 = one ? __ldg(g.erho + l0) : 0.f;
     const float er1 = two ? __ldg(g.erho + l0 + 1) : 0.f;
+    if constexpr (kFusedFirstPass<F>) {
+        if (F::kN == Lf) {
+            first_pass_gathered<F>(sm, G.tid, [&](int row) {
+                const FineRow fr = fine_row(g, cm, smm, __ldg(g.fine_cos + row), __ldg(g.fine_sin + row));
+                return make_float2(one ? gather_image(g, q, fr, vc, vr, er0) : 0.f,
+                                   two ? gather_image(g, q, fr, vc, vr, er1) : 0.f);
+            });
+            F::template run_tail<false>(sm, fd, G.tid);
+            float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
+            store_half_spectra<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out);
+            return;
+        }
+    }
+    for (int i = G.tid; i < Lf / 4; i += G.size) {  // the zero half [nf/2, Lf - nf/2)
+        sm[F::idx(nf / 2 + i)] = make_float2(0.f, 0.f);
+        sm[F::idx(nf / 2 + Lf / 4 + i)] = make_float2(0.f, 0.f);
+    }
     const int half_rows = nf / 2;
     for (int i = G.tid; i < half_rows; i += G.size) {
         const int i2 = i + half_rows;
@@ -563,11 +614,30 @@ __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, cons
     const int m = blockIdx.y, b = blockIdx.z;
     const int l0b = 2 * F::kP * blockIdx.x, l0 = l0b + 2 * G.g;
     const int nts = g.nts, L2 = g.L2, N = g.N;
-    for (int i = G.tid; i < nts; i += G.size) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
     const bool one = l0 < g.n_rho, two = l0 + 1 < g.n_rho;
     const float er0 = one ? __ldg(g.erho + l0) : 0.f;
     const float er1 = two ? __ldg(g.erho + l0 + 1) : 0.f;
     const float halfN = 0.5f * N;
+    if constexpr (kFusedFirstPass<F>) {
+        if (F::kN == L2) {
+            first_pass_gathered<F>(sm, G.tid, [&](int jj) {
+                const int j = jj - nts / 2;
+                int i = m * nts + j;
+                const bool flip = i < 0;
+                if (flip) i += g.n_theta;
+                const float* row = qg + (size_t(b) * g.n_theta + i) * N;
+                const float cth = __ldg(g.coarse_cos + jj) * g.one_m_aR;
+                const float sg = flip ? -halfN : halfN;
+                return make_float2(one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN)) : 0.f,
+                                   two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN)) : 0.f);
+            });
+            F::template run_tail<false>(sm, fd, G.tid);
+            float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * g.n_rho;
+            store_half_spectra<F>(Slots{smem, E}, L2, nts, g.n_rho, l0b, out);
+            return;
+        }
+    }
+    for (int i = G.tid; i < nts; i += G.size) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
     // two lattice rows per iteration (jj and jj + nts/2) for more loads in flight
     for (int jh = G.tid; jh < nts / 2; jh += G.size) {
         float v[2][2];
