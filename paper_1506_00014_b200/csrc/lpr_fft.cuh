@@ -54,12 +54,14 @@ __device__ __forceinline__ float2 mul_mi(float2 a) {
     return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
 }
 
-// R-point DFT in registers, sign -1 (forward) or +1 (INV).
+// R-point DFT in registers, sign -1 (forward) or +1 (INV). Output k is left
+// in register slot(k) (identity here; composite radices permute).
 template <int R, bool INV>
 struct Dft;
 
 template <bool INV>
 struct Dft<2, INV> {
+    __host__ __device__ static constexpr int slot(int k) { return k; }
     __device__ __forceinline__ static void run(float2* v) {
         const float2 a = v[0], b = v[1];
         v[0] = cadd(a, b);
@@ -69,6 +71,7 @@ struct Dft<2, INV> {
 
 template <bool INV>
 struct Dft<4, INV> {
+    __host__ __device__ static constexpr int slot(int k) { return k; }
     __device__ __forceinline__ static void run(float2* v) {
         const float2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
         const float2 s13 = cadd(v[1], v[3]), d13 = mul_mi<INV>(csub(v[1], v[3]));
@@ -81,6 +84,7 @@ struct Dft<4, INV> {
 
 template <bool INV>
 struct Dft<8, INV> {
+    __host__ __device__ static constexpr int slot(int k) { return k; }
     __device__ __forceinline__ static void run(float2* v) {
         constexpr float h = 0.70710678118654752f;
         float2 e[4] = {v[0], v[2], v[4], v[6]};
@@ -130,6 +134,7 @@ __device__ __forceinline__ const Roots<7>& roots<7>() { return c_roots7; }
 
 template <int R, bool INV>
 struct DftOdd {
+    __host__ __device__ static constexpr int slot(int k) { return k; }
     __device__ __forceinline__ static void run(float2* v) {
         const Roots<R>& rt = roots<R>();
         float2 out[R];
@@ -152,6 +157,7 @@ struct DftOdd {
 // radix 3: X0 = v0 + t1, X1,2 = (v0 - t1/2) -/+ i (sqrt3/2) t2 (forward), t1 = v1 + v2, t2 = v1 - v2
 template <bool INV>
 struct Dft<3, INV> {
+    __host__ __device__ static constexpr int slot(int k) { return k; }
     __device__ __forceinline__ static void run(float2* v) {
         constexpr float s = 0.86602540378443865f;
         const float2 t1 = cadd(v[1], v[2]);

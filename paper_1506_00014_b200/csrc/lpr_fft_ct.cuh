@@ -48,7 +48,7 @@ LPR_WR(32)
 template <int P, int Q, bool INV>
 __device__ __forceinline__ void dft_pq(float2* v) {
     constexpr int R = P * Q;
-    float2 y[Q][P];
+    // in place: P-point DFTs over n1 leave Y(n2, k1) in v[Q k1 + n2]
 #pragma unroll
     for (int n2 = 0; n2 < Q; ++n2) {
         float2 t[P];
@@ -56,50 +56,41 @@ __device__ __forceinline__ void dft_pq(float2* v) {
         for (int n1 = 0; n1 < P; ++n1) t[n1] = v[Q * n1 + n2];
         Dft<P, INV>::run(t);
 #pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) y[n2][k1] = t[k1];
+        for (int k1 = 0; k1 < P; ++k1) v[Q * k1 + n2] = t[Dft<P, INV>::slot(k1)];
     }
 #pragma unroll
-    for (int n2 = 1; n2 < Q; ++n2)
+    for (int k1 = 1; k1 < P; ++k1)
 #pragma unroll
-        for (int k1 = 1; k1 < P; ++k1) {
+        for (int n2 = 1; n2 < Q; ++n2) {
             const float2 w = wr<R>((n2 * k1) % R);
-            y[n2][k1] = INV ? cmulc(y[n2][k1], w) : cmul(y[n2][k1], w);
+            v[Q * k1 + n2] = INV ? cmulc(v[Q * k1 + n2], w) : cmul(v[Q * k1 + n2], w);
         }
+    // Q-point DFTs over n2: X(k1 + P k2) -> v[Q k1 + k2]
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) {
         float2 t[Q];
 #pragma unroll
-        for (int n2 = 0; n2 < Q; ++n2) t[n2] = y[n2][k1];
+        for (int n2 = 0; n2 < Q; ++n2) t[n2] = v[Q * k1 + n2];
         Dft<Q, INV>::run(t);
 #pragma unroll
-        for (int k2 = 0; k2 < Q; ++k2) v[k1 + P * k2] = t[k2];
+        for (int k2 = 0; k2 < Q; ++k2) v[Q * k1 + k2] = t[Dft<Q, INV>::slot(k2)];
     }
 }
 
-template <bool INV>
-struct Dft<6, INV> {
-    __device__ __forceinline__ static void run(float2* v) { dft_pq<2, 3, INV>(v); }
-};
-template <bool INV>
-struct Dft<9, INV> {
-    __device__ __forceinline__ static void run(float2* v) { dft_pq<3, 3, INV>(v); }
-};
-template <bool INV>
-struct Dft<12, INV> {
-    __device__ __forceinline__ static void run(float2* v) { dft_pq<4, 3, INV>(v); }
-};
-template <bool INV>
-struct Dft<16, INV> {
-    __device__ __forceinline__ static void run(float2* v) { dft_pq<4, 4, INV>(v); }
-};
-template <bool INV>
-struct Dft<27, INV> {
-    __device__ __forceinline__ static void run(float2* v) { dft_pq<3, 9, INV>(v); }
-};
-template <bool INV>
-struct Dft<32, INV> {
-    __device__ __forceinline__ static void run(float2* v) { dft_pq<4, 8, INV>(v); }
-};
+// Composite radix R = P Q, in place: output k sits in slot Q (k mod P) + k / P.
+#define LPR_DFT_PQ(RR, PP, QQ)                                                               \
+    template <bool INV>                                                                      \
+    struct Dft<RR, INV> {                                                                    \
+        __host__ __device__ static constexpr int slot(int k) { return QQ * (k % PP) + k / PP; } \
+        __device__ __forceinline__ static void run(float2* v) { dft_pq<PP, QQ, INV>(v); }    \
+    };
+LPR_DFT_PQ(6, 2, 3)
+LPR_DFT_PQ(9, 3, 3)
+LPR_DFT_PQ(12, 4, 3)
+LPR_DFT_PQ(16, 4, 4)
+LPR_DFT_PQ(27, 3, 9)
+LPR_DFT_PQ(32, 4, 8)
+#undef LPR_DFT_PQ
 
 // Padded shared index: one spare slot every 2^S elements (S = 0: none). The
 // best S per plan comes from a bank-conflict count of every pass's read and
@@ -145,7 +136,7 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
             Dft<R, INV>::run(v[i]);
             const int base = (b - k) * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[ct_pad<S>(base + r * NS)] = v[i][r];
+            for (int r = 0; r < R; ++r) x[ct_pad<S>(base + r * NS)] = v[i][Dft<R, INV>::slot(r)];
         }
     }
     __syncthreads();
@@ -242,7 +233,7 @@ struct GenericFft {
 //                   N      T   P  minB pad radices
 using Fft2048 = CtFft<2048, 128, 4, 2, 4, 16, 16, 8>;
 using Fft4096 = CtFft<4096, 256, 2, 1, 4, 16, 16, 16>;
-using Fft4374 = CtFft<4374, 192, 1, 2, 0, 27, 27, 6>;
+using Fft4374 = CtFft<4374, 192, 1, 4, 0, 27, 27, 6>;
 using Fft8192 = CtFft<8192, 512, 1, 2, 4, 16, 16, 16, 2>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 

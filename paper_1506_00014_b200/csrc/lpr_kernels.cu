@@ -420,7 +420,7 @@ __device__ __forceinline__ void first_pass_gathered(float2* sm, int tid, Gather&
             }
             Dft<R1, false>::run(v);
 #pragma unroll
-            for (int r = 0; r < R1; ++r) sm[F::idx(bb * R1 + r)] = v[r];
+            for (int r = 0; r < R1; ++r) sm[F::idx(bb * R1 + r)] = v[Dft<R1, false>::slot(r)];
         }
     }
     __syncthreads();
