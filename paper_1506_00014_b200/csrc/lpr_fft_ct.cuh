@@ -234,7 +234,10 @@ struct GenericFft {
 using Fft2048 = CtFft<2048, 128, 4, 2, 4, 16, 16, 8>;
 using Fft4096 = CtFft<4096, 256, 2, 1, 4, 16, 16, 16>;
 using Fft4374 = CtFft<4374, 192, 1, 4, 0, 27, 27, 6>;
-using Fft8192 = CtFft<8192, 512, 1, 2, 4, 16, 16, 16, 2>;
+#ifndef LPR_FFT8192_P
+#define LPR_FFT8192_P 1  // column pairs per block of the fine theta kernels (A/B knob)
+#endif
+using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, (LPR_FFT8192_P == 1 ? 2 : 1), 4, 16, 16, 16, 2>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 
 }  // namespace lpr
