@@ -233,7 +233,7 @@ struct GenericFft {
 //                   N      T   P  minB pad radices
 using Fft2048 = CtFft<2048, 128, 4, 2, 4, 16, 16, 8>;
 using Fft4096 = CtFft<4096, 256, 2, 1, 4, 16, 16, 16>;
-using Fft4374 = CtFft<4374, 192, 1, 4, 0, 27, 27, 6>;
+using Fft4374 = CtFft<4374, 192, 1, 2, 0, 27, 27, 6>;
 #ifndef LPR_FFT8192_P
 #define LPR_FFT8192_P 1  // column pairs per block of the fine theta kernels (A/B knob)
 #endif

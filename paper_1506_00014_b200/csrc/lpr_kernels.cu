@@ -761,7 +761,7 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         const float cm = g.cosm[m], smm = g.sinm[m];
         const float yx = fmaf(g.aR, fmaf(cm, xp, smm * yp), g.one_m_aR);
         const float yy = g.aR * fmaf(-smm, xp, cm * yp);
-        const float th = atan2f(yy, yx);
+        const float th = atanf(__fdividef(yy, yx));  // yx >= 1 - 2 aR > 0 inside the unit disc
         const float rho = 0.5f * logf(fmaf(yx, yx, yy * yy));
         const float tt = th * g.inv_dtheta_p;
         const float tr = (rho - g.log_ar) * g.inv_drho;
@@ -769,21 +769,28 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         float wt[4], wr[4];
         bsw(tt - kt, wt);
         bsw(tr - kr, wr);
-        const float* base = lp + (size_t(b) * g.M + m) * size_t(g.win) * n;
-        const int r0 = int(kt) - 1 - g.j0;
-        int cidx[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            int idx = int(kr) - 1 + q;
-            cidx[q] = idx < 0 ? idx + n : (idx >= n ? idx - n : idx);
-        }
+        const float* base = lp + (size_t(b) * g.M + m) * size_t(g.win) * n + (int(kt) - 1 - g.j0) * n;
+        const int c0 = int(kr) - 1;
         float sacc = 0.f;
+        if (c0 >= 0 && c0 + 3 < n) {  // no rho wrap (all but the last columns)
+            const float* row = base + c0;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const float* row = base + size_t(r0 + a) * n;
-            const float v = fmaf(wr[0], __ldg(row + cidx[0]),
-                                 fmaf(wr[1], __ldg(row + cidx[1]), fmaf(wr[2], __ldg(row + cidx[2]), wr[3] * __ldg(row + cidx[3]))));
-            sacc = fmaf(wt[a], v, sacc);
+            for (int a = 0; a < 4; ++a, row += n)
+                sacc = fmaf(wt[a], fmaf(wr[0], __ldg(row), fmaf(wr[1], __ldg(row + 1), fmaf(wr[2], __ldg(row + 2), wr[3] * __ldg(row + 3)))), sacc);
+        } else {
+            int cidx[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int idx = c0 + q;
+                cidx[q] = idx < 0 ? idx + n : (idx >= n ? idx - n : idx);
+            }
+            const float* row = base;
+#pragma unroll
+            for (int a = 0; a < 4; ++a, row += n) {
+                const float v = fmaf(wr[0], __ldg(row + cidx[0]),
+                                     fmaf(wr[1], __ldg(row + cidx[1]), fmaf(wr[2], __ldg(row + cidx[2]), wr[3] * __ldg(row + cidx[3]))));
+                sacc = fmaf(wt[a], v, sacc);
+            }
         }
         acc += sacc;
     }
