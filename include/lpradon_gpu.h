@@ -70,6 +70,14 @@ int lpr_spectrum_quadrature(const lpr_geometry* geom, int kind, double* out_re_i
  * spectrum may be NULL, in which case it is computed here. */
 int lpr_gpu_plan_create(int device, const lpr_geometry* geom, const double* zeta_re_im,
                         const double* zeta_bp_re_im, int max_batch, lpr_gpu_plan** out);
+/* Plan flags. LPR_PLAN_TEXTURE_GATHER: the fine-grid gather of R uses
+ * hardware bilinear texture filtering (two linear lookups per axis,
+ * PAPER.md:332-349) instead of fp32 software taps — a measured ablation only
+ * (the texture unit's fixed-point weights cost ~1e-3 relative accuracy);
+ * radon_transpose is not defined for such a plan. */
+enum { LPR_PLAN_TEXTURE_GATHER = 1 };
+int lpr_gpu_plan_create_ex(int device, const lpr_geometry* geom, const double* zeta_re_im,
+                           const double* zeta_bp_re_im, int max_batch, unsigned flags, lpr_gpu_plan** out);
 void lpr_gpu_plan_destroy(lpr_gpu_plan* plan);
 
 /* Algorithm 1: d_img (batch x N x N) -> d_sino (batch x n_theta x N). */
@@ -79,6 +87,15 @@ int lpr_gpu_backproject(lpr_gpu_plan* plan, const float* d_sino, float* d_img, i
 /* Exact transpose of lpr_gpu_radon under <g,h>_Sigma = 2 dtheta ds sum(g h)
  * and <f,u>_X = sum(f u) / N^2, so <R f, g>_Sigma = <f, R^T g>_X. */
 int lpr_gpu_radon_transpose(lpr_gpu_plan* plan, const float* d_sino, float* d_img, int batch, void* stream);
+
+/* Filtered back-projection (the main caller of R#):
+ * kind 0 = ramp, 1 = Shepp-Logan, 2 = cosine transfer functions along s
+ * (discrete band-limited ramp with end-point correction, 2N zero padding).
+ * lpr_gpu_filter: d_in sinograms -> filtered sinograms (no normalisation);
+ * lpr_gpu_fbp: c_norm * R#(filter(d_sino)) with c_norm = 1/2. */
+int lpr_gpu_filter(lpr_gpu_plan* plan, int kind, const float* d_in, float* d_out, int batch, void* stream);
+int lpr_gpu_fbp(lpr_gpu_plan* plan, int kind, const float* d_sino, float* d_img, int batch, void* stream);
+int lpr_gpu_fbp_host(lpr_gpu_plan* plan, int kind, const float* h_sino, float* h_img, int batch);
 
 /* Same operators on host buffers: pinned staging, H2D, compute, D2H and a
  * stream synchronisation inside the call (the end-to-end path). */

@@ -244,6 +244,60 @@ def fft2d_count_reset() -> None:
     lib().lpo_fft2d_count_reset()
 
 
+# ----------------------------------------------------------------- FBP
+
+FILTER_KINDS = ("ramp", "shepp-logan", "cosine")
+
+
+def filter_spectrum(N: int, kind: str = "ramp") -> np.ndarray:
+    """Real, even transfer function on the 2N-point DFT grid used by
+    apply_filter, normalised so that filtered = IDFT(DFT(pad(g)) * H)[:N].
+
+    The ramp is the DFT of the band-limited discrete ramp kernel (Kak &
+    Slaney): h(0) = 1/(4 ds^2), h(n odd) = -1/(n pi ds)^2, h(n even) = 0,
+    times ds — this is the end-point corrected |sigma| whose sigma = 0 bin is
+    the trapezoid value of the discrete kernel rather than 0.
+    Shepp-Logan and cosine multiply it by sinc(sigma/N) and cos(pi sigma/N)
+    (the cosine variant that vanishes at sigma = N/2,
+    SPEC.md:377), sigma_k = k / (2 N ds) cycles per unit length."""
+    if kind not in FILTER_KINDS:
+        raise ValueError(f"unknown filter kind {kind!r}")
+    ds = 1.0 / N
+    n = np.arange(2 * N)
+    lag = np.where(n < N, n, n - 2 * N)
+    h = np.zeros(2 * N)
+    h[lag == 0] = 1.0 / (4 * ds * ds)
+    odd = (lag % 2) != 0
+    h[odd] = -1.0 / (np.pi * lag[odd] * ds) ** 2
+    H = np.real(np.fft.fft(h)) * ds
+    sigma = np.abs(np.where(n <= N, n, n - 2 * N)) / (2 * N * ds)
+    if kind == "shepp-logan":
+        H = H * np.sinc(sigma / N)
+    elif kind == "cosine":
+        H = H * np.cos(np.pi * sigma / N)
+    return H
+
+
+def apply_filter(sino: np.ndarray, kind: str = "ramp") -> np.ndarray:
+    """Per-theta-row linear convolution along s with 2N zero padding
+    (SPEC.md:353-361)."""
+    g = np.asarray(sino, dtype=np.float64)
+    N = g.shape[-1]
+    H = filter_spectrum(N, kind)
+    G = np.fft.fft(np.concatenate([g, np.zeros_like(g)], axis=-1), axis=-1)
+    return np.real(np.fft.ifft(G * H, axis=-1))[..., :N]
+
+
+# fbp = C_NORM * fast_backprojection(apply_filter(g)): R# integrates over the
+# full line set (factor 2, PAPER.md:190), the inversion formula over a half
+# turn, so C_NORM = 1/2; checked by the disc calibration of SPEC.md:368/378.
+C_NORM = 0.5
+
+
+def fbp(p: Plan, zeta_bp: np.ndarray, sino: np.ndarray, kind: str = "ramp") -> np.ndarray:
+    return C_NORM * fast_backprojection(p, zeta_bp, apply_filter(sino, kind))
+
+
 # ----------------------------------------------------------------- inputs
 
 def smooth_disc_image(N: int, support_radius: float, seed: int, blur_sigma: float = 3.0) -> np.ndarray:

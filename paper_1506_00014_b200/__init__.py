@@ -8,7 +8,9 @@ from .lp_ops import (  # noqa: F401
     Geometry,
     RadonPlan,
     adjoint_gap,
+    apply_filter,
     fast_backprojection,
+    fbp,
     fast_radon,
     inner_image,
     inner_sinogram,

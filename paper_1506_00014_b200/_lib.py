@@ -31,6 +31,9 @@ EXPORTS = {
     "lpr_spectrum_quadrature": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_void_p]),
     "lpr_gpu_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(Geometry), ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "lpr_gpu_plan_create_ex": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(Geometry), ctypes.c_void_p,
+                                              ctypes.c_void_p, ctypes.c_int, ctypes.c_uint,
+                                              ctypes.POINTER(ctypes.c_void_p)]),
     "lpr_gpu_plan_destroy": (None, [ctypes.c_void_p]),
     "lpr_gpu_radon": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                      ctypes.c_void_p]),
@@ -45,6 +48,11 @@ EXPORTS = {
     "lpr_gpu_profile_stages": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                               ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                               ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_char_p)]),
+    "lpr_gpu_filter": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                      ctypes.c_void_p]),
+    "lpr_gpu_fbp": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                   ctypes.c_void_p]),
+    "lpr_gpu_fbp_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "lpr_gpu_launch_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_fft_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_last_error": (ctypes.c_char_p, []),

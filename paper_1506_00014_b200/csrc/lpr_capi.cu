@@ -19,7 +19,6 @@ namespace lpr {
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
 __global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* img, Tap* q4);
-__global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float* img, Tap* q4);
 __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const float* sino, float* qg);
 __global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* sino, float* qg);
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
@@ -113,8 +112,10 @@ struct lpr_gpu_plan {
     lpr_geometry geo{};
     int max_batch = 1;
     DevGeom g{};
-    FftDesc d_fine{}, d_rho{}, d_coarse{};
-    FftLaunch l_fine{}, l_rho{}, l_coarse{};
+    FftDesc d_fine{}, d_rho{}, d_coarse{}, d_filt{};
+    FftLaunch l_fine{}, l_rho{}, l_coarse{}, l_filt{};
+    float* filt_tab = nullptr;  // 2 x 3 transfer functions of length 2N: [fbp?][kind][k], / 2N (fbp: x c_norm)
+    float* fsino = nullptr;     // filtered sinograms for fbp
     float2* mult_R = nullptr;
     float2* mult_B = nullptr;
     float2* mult_RT = nullptr;   // conj(mult_R): the transposed rho multiplier
@@ -129,6 +130,8 @@ struct lpr_gpu_plan {
     cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
+    bool tex_gather = false;      // LPR_PLAN_TEXTURE_GATHER ablation
+    cudaTextureObject_t qtex = 0;
     std::vector<void*> allocs;
     long long launches = 0, ffts = 0;
 
@@ -192,6 +195,7 @@ struct lpr_gpu_plan {
     }
 
     ~lpr_gpu_plan() {
+        if (qtex) cudaDestroyTextureObject(qtex);
         for (void* p : allocs) cudaFree(p);
         if (h_in) cudaFreeHost(h_in);
         if (h_out) cudaFreeHost(h_out);
@@ -270,6 +274,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     p->build_desc(g.Lf, p->d_fine, p->l_fine);
     p->build_desc(G.n_rho, p->d_rho, p->l_rho);
     p->build_desc(g.L2, p->d_coarse, p->l_coarse);
+    p->build_desc(2L * G.N, p->d_filt, p->l_filt);
 
     // spectral multipliers on the half theta spectrum k in [0, nts]
     const long nts = G.nts, nr = G.n_rho, rows = 2 * nts;
@@ -305,6 +310,43 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     for (auto& v : mr) v.y = -v.y;
     p->mult_RT = p->upload(mr);
 
+    // FBP transfer functions: DFT of the band-limited discrete
+    // ramp kernel h(0) = 1/(4 ds^2), h(odd n) = -1/(n pi ds)^2 times ds, windowed
+    // by sinc(sigma/N) (Shepp-Logan) or cos(pi sigma/N) (cosine); / 2N for the
+    // unnormalised inverse; the fbp copy also carries c_norm = 1/2 (R# integrates
+    // over all lines, the inversion over a half turn).
+    {
+        const long N = G.N, L = 2 * N;
+        const double ds = 1.0 / double(N);
+        std::vector<double> h(L, 0.0), ramp(L, 0.0);
+        for (long n = 0; n < L; ++n) {
+            const long lag = n < N ? n : n - L;
+            if (lag == 0) h[n] = 1.0 / (4.0 * ds * ds);
+            else if (lag % 2) h[n] = -1.0 / ((kPi * double(lag) * ds) * (kPi * double(lag) * ds));
+        }
+        for (long k = 0; k < L; ++k) {  // real, even kernel: cosine transform
+            double acc = 0.0;
+            for (long n = 0; n < L; ++n) acc += h[n] * std::cos(2.0 * kPi * double((k * n) % L) / double(L));
+            ramp[k] = acc * ds;
+        }
+        std::vector<float> tab(6 * L);
+        for (int kind = 0; kind < 3; ++kind)
+            for (long k = 0; k < L; ++k) {
+                const double sigma = double(k <= N ? k : L - k) / (double(L) * ds);
+                double w = 1.0;
+                if (kind == 1) {
+                    const double x = sigma / double(N);
+                    w = x == 0.0 ? 1.0 : std::sin(kPi * x) / (kPi * x);
+                } else if (kind == 2) {
+                    w = std::cos(kPi * sigma / double(N));
+                }
+                const double v = ramp[k] * w / double(L);
+                tab[kind * L + k] = float(v);
+                tab[(3 + kind) * L + k] = float(0.5 * v);
+            }
+        p->filt_tab = p->upload(tab);
+    }
+
     // Q1 (pitch x N): apron-extended FIR prefilter as the forward kernels apply
     // it (fp32 taps); band[c][j] = Q1[c + A - H + j][c] holds its transpose.
     {
@@ -338,6 +380,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     p->q4 = p->dalloc<Tap>(B * g.pitch * g.pitch);
     p->qf = reinterpret_cast<float*>(p->q4);
     p->qg = p->dalloc<float>(B * G.n_theta * G.N);
+    p->fsino = p->dalloc<float>(B * G.n_theta * G.N);
     p->spec = p->dalloc<float2>(B * G.M * (nts + 1) * nr);
     p->lp = p->dalloc<float>(B * G.M * g.win * nr);
     const size_t io = B * std::max<size_t>(size_t(G.N) * G.N, size_t(G.n_theta) * G.N);
@@ -354,8 +397,32 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         ck(cudaEventCreateWithFlags(&p->ev_d2h[i], cudaEventDisableTiming), "cudaEventCreate");
     }
 
+    ck(prepare_filter_kernel(p->l_filt), "filter smem attribute");
     ck(prepare_fft_kernels(p->l_fine, p->l_rho, p->l_coarse, size_t(G.n_rho) * sizeof(float2)),
        "fft smem attributes");
+    if (p->tex_gather) {
+        // the plain coefficient rasters of the whole batch as one tall pitched
+        // 2-D texture with hardware bilinear filtering
+        int align = 0;
+        ck(cudaDeviceGetAttribute(&align, cudaDevAttrTexturePitchAlignment, p->device), "device query");
+        const size_t pitch_bytes = size_t(g.pitch) * sizeof(float);
+        if (align <= 0 || pitch_bytes % size_t(align) != 0)
+            throw std::invalid_argument("texture gather: image row pitch not texture-aligned (use N divisible by 8)");
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypePitch2D;
+        rd.res.pitch2D.devPtr = p->qf;
+        rd.res.pitch2D.desc = cudaCreateChannelDesc<float>();
+        rd.res.pitch2D.width = size_t(g.pitch);
+        rd.res.pitch2D.height = size_t(g.pitch) * B;
+        rd.res.pitch2D.pitchInBytes = pitch_bytes;
+        cudaTextureDesc td{};
+        td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModeLinear;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        ck(cudaCreateTextureObject(&p->qtex, &rd, &td, nullptr), "cudaCreateTextureObject");
+        p->g.qtex = p->qtex;
+    }
     set_smem((const void*)k_radon_out, size_t(nr) * sizeof(float));
     set_smem((const void*)k_radon_out_T, size_t(nr) * sizeof(float));
 
@@ -370,9 +437,9 @@ inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
 void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
     mark(p, 0, st);
-    k_prefilter_2d_iir<<<dim3(cdiv(g.pitch, 64), cdiv(g.pitch, 64), nb), 128, 0, st>>>(g, img, p->q4);
+    launch_prefilter_2d(!p->tex_gather, nb, st, g, img, p->q4);
     mark(p, 1, st);
-    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->q4, p->spec);
+    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->q4, p->spec, p->tex_gather);
     mark(p, 2, st);
     launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_R, p->spec);
     mark(p, 3, st);
@@ -416,6 +483,22 @@ void transpose_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cud
     check_launch("radon transpose launch");
     p->launches += 6;
     p->ffts += 2LL * g.M * nb;
+}
+
+// FBP pieces: filter along s, then Algorithm 2.
+template <int KIND, bool FBP>
+void filter_chunk(lpr_gpu_plan* p, const float* sino, float* out, int nb, cudaStream_t st) {
+    const DevGeom& g = p->g;
+    const float* H = p->filt_tab + size_t((FBP ? 3 : 0) + KIND) * 2 * g.N;
+    launch_sino_filter(p->l_filt, nb * g.n_theta, st, g, p->d_filt, H, sino, out);
+    check_launch("filter launch");
+    p->launches += 1;
+}
+
+template <int KIND>
+void fbp_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
+    filter_chunk<KIND, true>(p, sino, p->fsino, nb, st);
+    backproject_chunk(p, p->fsino, img, nb, st);
 }
 
 const char* const kBackprojectStages[] = {"prefilter_sino", "bp_theta_fwd", "rho_pass", "theta_inv", "bp_out"};
@@ -525,7 +608,13 @@ int lpr_spectrum_quadrature(const lpr_geometry* geom, int kind, double* out) {
 
 int lpr_gpu_plan_create(int device, const lpr_geometry* geom, const double* zeta, const double* zeta_bp,
                         int max_batch, lpr_gpu_plan** out) {
+    return lpr_gpu_plan_create_ex(device, geom, zeta, zeta_bp, max_batch, 0u, out);
+}
+
+int lpr_gpu_plan_create_ex(int device, const lpr_geometry* geom, const double* zeta, const double* zeta_bp,
+                           int max_batch, unsigned flags, lpr_gpu_plan** out) {
     return guard([&] {
+        if (flags & ~unsigned(LPR_PLAN_TEXTURE_GATHER)) throw std::invalid_argument("plan: unknown flags");
         if (!geom || !out) throw std::invalid_argument("null argument");
         if (max_batch < 1) throw std::invalid_argument("max_batch must be >= 1");
         // re-derive so a hand-edited struct cannot desynchronise the tables
@@ -536,6 +625,7 @@ int lpr_gpu_plan_create(int device, const lpr_geometry* geom, const double* zeta
         p->device = device;
         p->geo = G;
         p->max_batch = max_batch;
+        p->tex_gather = (flags & LPR_PLAN_TEXTURE_GATHER) != 0;
         try {
             init_plan(p, zeta, zeta_bp);
         } catch (...) {
@@ -576,6 +666,38 @@ int lpr_gpu_backproject_host(lpr_gpu_plan* p, const float* h_sino, float* h_img,
     });
 }
 
+namespace {
+ChunkFn filter_fn(int kind, bool fbp) {
+    switch (kind) {
+        case 0: return fbp ? fbp_chunk<0> : filter_chunk<0, false>;
+        case 1: return fbp ? fbp_chunk<1> : filter_chunk<1, false>;
+        case 2: return fbp ? fbp_chunk<2> : filter_chunk<2, false>;
+        default: throw std::invalid_argument("filter kind must be 0 (ramp), 1 (shepp-logan) or 2 (cosine)");
+    }
+}
+}  // namespace
+
+int lpr_gpu_filter(lpr_gpu_plan* p, int kind, const float* d_in, float* d_out, int batch, void* stream) {
+    return guard([&] {
+        const size_t sz = size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0);
+        run_device(p, filter_fn(kind, false), d_in, d_out, batch, sz, sz, stream);
+    });
+}
+
+int lpr_gpu_fbp(lpr_gpu_plan* p, int kind, const float* d_sino, float* d_img, int batch, void* stream) {
+    return guard([&] {
+        run_device(p, filter_fn(kind, true), d_sino, d_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
+                   size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream);
+    });
+}
+
+int lpr_gpu_fbp_host(lpr_gpu_plan* p, int kind, const float* h_sino, float* h_img, int batch) {
+    return guard([&] {
+        run_host(p, filter_fn(kind, true), h_sino, h_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
+                 size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0));
+    });
+}
+
 int lpr_gpu_radon_transpose_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batch) {
     return guard([&] {
         run_host(p, transpose_chunk, h_sino, h_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
@@ -585,6 +707,7 @@ int lpr_gpu_radon_transpose_host(lpr_gpu_plan* p, const float* h_sino, float* h_
 
 int lpr_gpu_radon_transpose(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, void* stream) {
     return guard([&] {
+        if (p && p->tex_gather) throw std::invalid_argument("radon_transpose: not defined for a texture-gather plan");
         run_device(p, transpose_chunk, d_sino, d_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
                    size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream);
     });

@@ -126,7 +126,8 @@ constexpr int kIR = kIT + 2 * kIW;        // staged rows
 constexpr int kIC = kIT + 3 + 2 * kIW;    // staged columns (quad needs 3 more)
 constexpr int kICP = kIC + 2;             // odd row pitch (101): row- and column-walks are conflict-free
 
-__global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float* __restrict__ img, Tap* __restrict__ q4) {
+template <class T>
+__global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float* __restrict__ img, T* __restrict__ q4) {
     __shared__ float s[kIR][kICP];
     constexpr float z = -0.26794919243112270647f;
     constexpr float c0 = 6.0f / (1.0f - z), ca = -z / (1.0f - z);
@@ -160,17 +161,26 @@ __global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float
         for (int k = kIR - 2; k >= 0; --k) s[k][j] = d = z * (d - s[k][j]);
     }
     __syncthreads();
-    Tap* dst = q4 + size_t(b) * pitch * pitch;
+    T* dst = q4 + size_t(b) * pitch * pitch;
     for (int idx = tid; idx < kIT * kIT; idx += blockDim.x) {
         const int i = idx / kIT, j = idx % kIT;
         if (y0 + i >= pitch || x0 + j >= pitch) continue;
         const float* r = s[kIW + i] + kIW + j;
-#if LPR_TAPS == 4
-        dst[size_t(y0 + i) * pitch + x0 + j] = make_float4(r[0], r[1], r[2], r[3]);
-#else
-        dst[size_t(y0 + i) * pitch + x0 + j] = r[0];
-#endif
+        if constexpr (sizeof(T) == sizeof(float4)) {
+            dst[size_t(y0 + i) * pitch + x0 + j] = make_float4(r[0], r[1], r[2], r[3]);
+        } else {
+            dst[size_t(y0 + i) * pitch + x0 + j] = r[0];
+        }
     }
+}
+
+// quad = false writes the plain fp32 coefficient raster (the texture ablation binds it).
+void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out) {
+    const dim3 grid((g.pitch + kIT - 1) / kIT, (g.pitch + kIT - 1) / kIT, nb);
+    if (quad)
+        k_prefilter_2d_iir<Tap><<<grid, 128, 0, st>>>(g, img, static_cast<Tap*>(out));
+    else
+        k_prefilter_2d_iir<float><<<grid, 128, 0, st>>>(g, img, static_cast<float*>(out));
 }
 
 // Recursive prefilter along s for R# (Alg. 2 step 1): a 32-row x 256-column
@@ -429,11 +439,34 @@ __device__ __forceinline__ void first_pass_gathered(float2* sm, int tid, Gather&
 template <class F>
 constexpr bool kFusedFirstPass = F::kT > 0 && (F::kN % 4 == 0);
 
+// Texture-filtered ablation of gather_image: the cubic
+// spline as two hardware-bilinear lookups per axis, 4 filtered fetches per
+// sample from the plain coefficient raster bound as a pitched 2-D texture
+// (slice b at rows b * pitch). The texture unit quantises the interpolation
+// weights (9-bit fixed point), so this is ~1e-3 accurate, not 1e-4.
+__device__ __forceinline__ float gather_tex(const DevGeom& g, const FineRow& r, float vc, float vr, float er, int b) {
+    float tc, tr;
+    if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
+    const float kc = floorf(tc), kr = floorf(tr);
+    float wc[4], wr[4];
+    bsw(tc - kc, wc);
+    bsw(tr - kr, wr);
+    const float gc0 = wc[0] + wc[1], gc1 = wc[2] + wc[3], gr0 = wr[0] + wr[1], gr1 = wr[2] + wr[3];
+    const float x0 = kc + float(kApron - 1) + __fdividef(wc[1], gc0) + 0.5f;
+    const float x1 = kc + float(kApron + 1) + __fdividef(wc[3], gc1) + 0.5f;
+    const float yb = float(b * g.pitch) + kr + 0.5f;
+    const float y0 = yb + float(kApron - 1) + __fdividef(wr[1], gr0);
+    const float y1 = yb + float(kApron + 1) + __fdividef(wr[3], gr1);
+    const float top = fmaf(gc0, tex2D<float>(g.qtex, x0, y0), gc1 * tex2D<float>(g.qtex, x1, y0));
+    const float bot = fmaf(gc0, tex2D<float>(g.qtex, x0, y1), gc1 * tex2D<float>(g.qtex, x1, y1));
+    return er * fmaf(gr0, top, gr1 * bot);
+}
+
 // Alg. 1 steps 3-6a: gather T_m f e^rho on the fine grid of two rho columns,
 // zero-embed into the doubled fine period Lf, real theta FFT, keep |k| < nts.
 // Each thread gathers two fine rows per iteration (64 independent tap loads
 // in flight) to hide the L2 latency of the spline taps.
-template <class F>
+template <class F, bool TEX = false>
 __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                             const Tap* __restrict__ qf, float2* __restrict__ spec) {
     extern __shared__ float2 smem[];
@@ -452,8 +485,12 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         if (F::kN == Lf) {
             first_pass_gathered<F>(sm, G.tid, [&](int row) {
                 const FineRow fr = fine_row(g, cm, smm, __ldg(g.fine_cos + row), __ldg(g.fine_sin + row));
-                return make_float2(one ? gather_image(g, q, fr, vc, vr, er0) : 0.f,
-                                   two ? gather_image(g, q, fr, vc, vr, er1) : 0.f);
+                if constexpr (TEX)
+                    return make_float2(one ? gather_tex(g, fr, vc, vr, er0, b) : 0.f,
+                                       two ? gather_tex(g, fr, vc, vr, er1, b) : 0.f);
+                else
+                    return make_float2(one ? gather_image(g, q, fr, vc, vr, er0) : 0.f,
+                                       two ? gather_image(g, q, fr, vc, vr, er1) : 0.f);
             });
             F::template run_tail<false>(sm, fd, G.tid);
             float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
@@ -470,10 +507,18 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         const int i2 = i + half_rows;
         const FineRow r1 = fine_row(g, cm, smm, __ldg(g.fine_cos + i), __ldg(g.fine_sin + i));
         const FineRow r2 = fine_row(g, cm, smm, __ldg(g.fine_cos + i2), __ldg(g.fine_sin + i2));
-        const float h0 = one ? gather_image(g, q, r1, vc, vr, er0) : 0.f;
-        const float h1 = two ? gather_image(g, q, r1, vc, vr, er1) : 0.f;
-        const float h2 = one ? gather_image(g, q, r2, vc, vr, er0) : 0.f;
-        const float h3 = two ? gather_image(g, q, r2, vc, vr, er1) : 0.f;
+        float h0, h1, h2, h3;
+        if constexpr (TEX) {
+            h0 = one ? gather_tex(g, r1, vc, vr, er0, b) : 0.f;
+            h1 = two ? gather_tex(g, r1, vc, vr, er1, b) : 0.f;
+            h2 = one ? gather_tex(g, r2, vc, vr, er0, b) : 0.f;
+            h3 = two ? gather_tex(g, r2, vc, vr, er1, b) : 0.f;
+        } else {
+            h0 = one ? gather_image(g, q, r1, vc, vr, er0) : 0.f;
+            h1 = two ? gather_image(g, q, r1, vc, vr, er1) : 0.f;
+            h2 = one ? gather_image(g, q, r2, vc, vr, er0) : 0.f;
+            h3 = two ? gather_image(g, q, r2, vc, vr, er1) : 0.f;
+        }
         sm[F::idx(i - nf / 2 + Lf)] = make_float2(h0, h1);  // q = i - nf/2 < 0
         sm[F::idx(i2 - nf / 2)] = make_float2(h2, h3);      // q = i2 - nf/2 >= 0
     }
@@ -743,6 +788,40 @@ __global__ void LPR_LB(F) k_theta_inv_fine_T(const __grid_constant__ DevGeom g, 
     }
 }
 
+// FBP filter along s (the caller of R# in fbp):
+// two sinogram rows per complex transform of length 2N (zero padded, so the
+// circular convolution is the linear one on [0, N)), times the real even
+// transfer H (already divided by 2N); both packed rows see the same real H.
+template <class F>
+__global__ void LPR_LB(F) k_sino_filter(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                        const float* __restrict__ H, const float* __restrict__ in,
+                                        float* __restrict__ out, int rows_total) {
+    extern __shared__ float2 smem[];
+    const Group<F> G;
+    const int E = F::elems(fd);
+    float2* sm = smem + G.g * E;
+    const int r0 = 2 * (blockIdx.x * F::kP + G.g), N = g.N, L = 2 * N;
+    const bool has0 = r0 < rows_total, has1 = r0 + 1 < rows_total;
+    for (int j = G.tid; j < L; j += G.size) {
+        float a = 0.f, c = 0.f;
+        if (j < N) {
+            if (has0) a = __ldg(in + size_t(r0) * N + j);
+            if (has1) c = __ldg(in + size_t(r0 + 1) * N + j);
+        }
+        sm[F::idx(j)] = make_float2(a, c);
+    }
+    __syncthreads();
+    float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
+    for (int j = G.tid; j < L; j += G.size) a[F::idx(j)] = cscale(a[F::idx(j)], __ldg(H + j));
+    __syncthreads();
+    a = F::template run<true>(a, a == sm ? fft_scratch<F>(sm, fd) : sm, fd, G.tid);
+    for (int j = G.tid; j < N; j += G.size) {
+        const float2 v = a[F::idx(j)];
+        if (has0) out[size_t(r0) * N + j] = v.x;
+        if (has1) out[size_t(r0 + 1) * N + j] = v.y;
+    }
+}
+
 // T_m^{-1} Omega_p -> X resampling and the sector sum (Alg. 2 steps 5-7).
 __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restrict__ img) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -853,7 +932,10 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
         cudaError_t r = smem_attr((const void*)K, L);                          \
         if (r != cudaSuccess) e = r;                                           \
     } while (0)
-#define FINE(F) SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block); SET(k_theta_inv_fine_T<F>, fine.smem * fine.per_block)
+#define FINE(F)                                                   \
+    SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block);         \
+    SET((k_radon_theta_fwd<F, true>), fine.smem * fine.per_block); \
+    SET(k_theta_inv_fine_T<F>, fine.smem * fine.per_block)
 #define RHO(F) SET(k_rho_pass<F>, rho.smem + rho_mult_bytes)
 #define COARSE(F)                                          \
     SET(k_theta_inv<F>, coarse.smem * coarse.per_block);    \
@@ -870,7 +952,13 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 }
 
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const Tap* qf, float2* spec) {
+                            const Tap* qf, float2* spec, bool tex) {
+    if (tex) {
+#define CALL(F) k_radon_theta_fwd<F, true><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
+        LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+        return;
+    }
 #define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
@@ -900,6 +988,26 @@ void launch_bp_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const D
 void launch_theta_fwd_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                         const float* lp, float2* spec) {
 #define CALL(F) k_theta_fwd_T<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, lp, spec)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+}
+
+cudaError_t prepare_filter_kernel(const FftLaunch& L) {
+    cudaError_t e = cudaSuccess;
+#define SETF(F)                                                                            \
+    do {                                                                                   \
+        cudaError_t r = smem_attr((const void*)k_sino_filter<F>, L.smem * L.per_block);    \
+        if (r != cudaSuccess) e = r;                                                       \
+    } while (0)
+    LPR_FFT_SWITCH(L.variant, SETF)
+#undef SETF
+    return e;
+}
+
+void launch_sino_filter(const FftLaunch& L, int rows_total, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                        const float* H, const float* in, float* out) {
+    const dim3 grid((((rows_total + 1) / 2) + L.per_block - 1) / L.per_block);
+#define CALL(F) k_sino_filter<F><<<grid, L.threads, L.smem * L.per_block, st>>>(g, fd, H, in, out, rows_total)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }

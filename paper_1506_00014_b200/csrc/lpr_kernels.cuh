@@ -45,6 +45,7 @@ struct DevGeom {
     const float* coarse_cos;  // nts entries: cos(j dtheta_p), j = jj - nts/2
     const float* erho;        // n_rho entries: exp(log a_r + l drho)
     const float* fir;         // 2 kFirHalf + 1 prefilter taps
+    cudaTextureObject_t qtex; // texture-gather ablation: coefficient raster (0 unless enabled)
 };
 
 // FFT kernel variants: a compile-time register FFT for the hot lengths
@@ -64,7 +65,8 @@ std::vector<float2> fft_pass_twiddles(int variant);
 cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
                                 size_t rho_mult_bytes);
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const Tap* qf, float2* spec);
+                            const Tap* qf, float2* spec, bool tex);
+void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out);
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec);
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
@@ -75,5 +77,8 @@ void launch_theta_fwd_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const De
                         const float* lp, float2* spec);
 void launch_theta_inv_fine_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                              const float2* spec, float* qbar);
+cudaError_t prepare_filter_kernel(const FftLaunch& L);
+void launch_sino_filter(const FftLaunch& L, int rows_total, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                        const float* H, const float* in, float* out);
 
 }  // namespace lpr

@@ -59,7 +59,8 @@ class RadonPlan:
     """Immutable per-device plan: geometry, uploaded spectra, scratch for
     ``max_batch`` slices (larger batches run in chunks)."""
 
-    def __init__(self, geometry: Geometry, zeta=None, zeta_bp=None, max_batch: int = 1, device: int = 0):
+    def __init__(self, geometry: Geometry, zeta=None, zeta_bp=None, max_batch: int = 1, device: int = 0,
+                 texture_gather: bool = False):
         self.geometry = geometry
         self.max_batch = int(max_batch)
         self.device = int(device)
@@ -69,10 +70,11 @@ class RadonPlan:
             if a is not None and a.shape != (2 * geometry.nts, geometry.n_rho):
                 raise ValueError(f"spectrum shape {a.shape} does not match the plan")
         h = ctypes.c_void_p()
-        check(lib().lpr_gpu_plan_create(self.device, ctypes.byref(geometry),
-                                        None if z is None else z.ctypes.data,
-                                        None if zb is None else zb.ctypes.data,
-                                        self.max_batch, ctypes.byref(h)))
+        self.texture_gather = bool(texture_gather)
+        check(lib().lpr_gpu_plan_create_ex(self.device, ctypes.byref(geometry),
+                                           None if z is None else z.ctypes.data,
+                                           None if zb is None else zb.ctypes.data,
+                                           self.max_batch, 1 if texture_gather else 0, ctypes.byref(h)))
         self._h = h
 
     @property
@@ -166,6 +168,36 @@ def radon_transpose(sino, plan: RadonPlan):
     g = plan.geometry
     return _run(plan, sino, (g.n_theta, g.N), (g.N, g.N), lib().lpr_gpu_radon_transpose,
                 lib().lpr_gpu_radon_transpose_host)
+
+
+FILTER_KINDS = {"ramp": 0, "shepp-logan": 1, "cosine": 2}
+
+
+def _kind(kind: str) -> int:
+    if kind not in FILTER_KINDS:
+        raise ValueError(f"unknown filter kind {kind!r} (ramp, shepp-logan, cosine)")
+    return FILTER_KINDS[kind]
+
+
+def apply_filter(sino, plan: RadonPlan, kind: str = "ramp"):
+    """FBP filter along s: per-row linear convolution with the
+    discrete band-limited ramp (optionally Shepp-Logan / cosine windowed)."""
+    g, k = plan.geometry, _kind(kind)
+    if not (_is_torch(sino) and sino.is_cuda):
+        import torch
+
+        t = torch.as_tensor(np.ascontiguousarray(sino, dtype=np.float32), device=f"cuda:{plan.device}")
+        return apply_filter(t, plan, kind).cpu().numpy()
+    return _run(plan, sino, (g.n_theta, g.N), (g.n_theta, g.N),
+                lambda h, i, o, b, s: lib().lpr_gpu_filter(h, k, i, o, b, s), None)
+
+
+def fbp(sino, plan: RadonPlan, kind: str = "ramp"):
+    """Filtered back-projection: c_norm R#(filter(g)), c_norm = 1/2."""
+    g, k = plan.geometry, _kind(kind)
+    return _run(plan, sino, (g.n_theta, g.N), (g.N, g.N),
+                lambda h, i, o, b, s: lib().lpr_gpu_fbp(h, k, i, o, b, s),
+                lambda h, i, o, b: lib().lpr_gpu_fbp_host(h, k, i, o, b))
 
 
 def inner_sinogram(g: Geometry, a, b) -> float:

@@ -197,3 +197,82 @@ def test_cpp_dropin_against_reference_blocks(cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "adjoint gap" in r.stdout
+
+
+@pytest.mark.parametrize("kind", ["ramp", "shepp-logan", "cosine"])
+def test_fbp_parity_n512(lp, lpo, cuda, kind):
+    """Config 2 (N=512, 768 angles): the FBP filter and FBP against the oracle."""
+    import torch
+
+    N = 512
+    g, p, z, zb, plan = _setup(lp, lpo, N, lp.smooth_n_rho(N))
+    s = lpo.phantom_sinogram(p)
+    want_f = lpo.apply_filter(s, kind)
+    got_f = lp.apply_filter(torch.tensor(s, dtype=torch.float32, device=cuda), plan, kind).cpu().numpy()
+    assert lpo.rel_l2(got_f, want_f) <= TOL
+    want = lpo.fbp(p, zb, s, kind)
+    got = lp.fbp(torch.tensor(s, dtype=torch.float32, device=cuda), plan, kind).cpu().numpy()
+    assert lpo.rel_l2(got, want) <= TOL
+    host = lp.fbp(s.astype(np.float32), plan, kind)
+    np.testing.assert_array_equal(host, got)
+
+
+def test_texture_gather_ablation(lp, lpo, cuda):
+    """Config 5 ablation: hardware bilinear texture filtering in R's gather is
+    measurably less accurate than the fp32 software taps (its 9-bit weights)."""
+    import torch
+
+    N = 512
+    g, p, z, zb, soft = _setup(lp, lpo, N, lp.smooth_n_rho(N))
+    tex = lp.RadonPlan(g, z, zb, texture_gather=True)
+    f = lpo.smooth_disc_image(N, 0.9, 21)
+    want = lpo.fast_radon(p, z, f)
+    t = torch.tensor(f, dtype=torch.float32, device=cuda)
+    e_soft = lpo.rel_l2(lp.fast_radon(t, soft).cpu().numpy(), want)
+    e_tex = lpo.rel_l2(lp.fast_radon(t, tex).cpu().numpy(), want)
+    assert e_soft <= TOL
+    assert e_soft < e_tex <= 5e-3, (e_soft, e_tex)
+    with pytest.raises(ValueError):
+        lp.radon_transpose(torch.zeros(g.n_theta, N, device=cuda), tex)
+
+
+def test_config5_n4096(lp, lpo, cuda):
+    """Config 5 (N=4096, 6144 angles): R of a centred disc is rotation
+    invariant and matches 2 sqrt(r^2 - s^2); R# R keeps the disc's symmetry."""
+    import torch
+
+    N = 4096
+    g = lp.sampling_plan(N, 3, 0, lp.smooth_n_rho(N))
+    assert g.n_theta == 6144
+    plan = lp.RadonPlan(g, max_batch=1)
+    x = (np.arange(N) - N / 2) / N
+    rad = np.hypot(x[None, :], x[:, None])
+    f = torch.tensor((rad <= 0.2).astype(np.float32), device=cuda)
+    s = lp.fast_radon(f, plan).cpu().numpy().astype(np.float64)
+    want = 2 * np.sqrt(np.clip(0.04 - x ** 2, 0, None))
+    assert lpo.rel_l2(s.mean(axis=0), want) <= 5e-3
+    assert np.abs(s - s.mean(axis=0)).max() <= 1e-2 * want.max()
+    b = lp.fast_backprojection(torch.tensor(s, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    assert np.isfinite(b).all()
+    assert lpo.rel_l2(b, b[::-1, ::-1]) <= 1e-2  # point symmetry of a centred disc (up to the raster offset)
+
+
+def test_fbp_reconstructs_phantom(lp, lpo, cuda):
+    """FBP of the analytic Shepp-Logan sinogram at N=512 approximates the phantom
+    inside the head (ramp); disc calibration gives unit interior mean."""
+    import torch
+
+    N = 512
+    g = lp.sampling_plan(N, 3, 0, lp.smooth_n_rho(N))
+    plan = lp.RadonPlan(g)
+    p = lpo.make_plan(N, 3, 0, g.n_rho)
+    x = (np.arange(N) - N / 2) / N
+    rad = np.hypot(x[None, :], x[:, None])
+    s = -0.5 + np.arange(N) / N
+    disc = np.where(np.abs(s) < 0.25, 2 * np.sqrt(np.clip(0.0625 - s * s, 0, None)), 0.0)[None].repeat(g.n_theta, 0)
+    img = lp.fbp(torch.tensor(disc, dtype=torch.float32, device=cuda), plan, "ramp").cpu().numpy()
+    assert 0.98 <= img[rad < 0.2].mean() <= 1.02
+    ph = lpo.phantom_image(N)
+    rec = lp.fbp(torch.tensor(lpo.phantom_sinogram(p), dtype=torch.float32, device=cuda), plan, "cosine").cpu().numpy()
+    inside = rad < 0.4
+    assert lpo.rel_l2(rec[inside], ph[inside]) <= 0.25
