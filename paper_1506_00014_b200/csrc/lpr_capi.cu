@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <cstring>
 #include <stdexcept>
@@ -149,7 +150,8 @@ struct lpr_gpu_plan {
         return p;
     }
 
-    void build_desc(long n, FftDesc& d, FftLaunch& launch) {
+    // staged_row: the rho pass also stages one multiplier row (n float2) in shared memory
+    void build_desc(long n, FftDesc& d, FftLaunch& launch, bool staged_row = false) {
         d = FftDesc{};
         d.n = int(n);
         auto rad = radices(n);
@@ -190,7 +192,16 @@ struct lpr_gpu_plan {
         }
         launch = fft_launch_config(d);
         if (launch.variant != kFftGeneric) d.twp = upload(fft_pass_twiddles(launch.variant));
-        if (launch.smem * launch.per_block > 227 * 1024 || launch.smem + size_t(n) * sizeof(float2) > 227 * 1024)
+        // rho pass: the TMA-streamed kernel where one exists for this length
+        // (LPR_RHO_STREAM=0 selects the one-block-per-row kernel, for A/B runs)
+        const char* rs = std::getenv("LPR_RHO_STREAM");
+        if (staged_row && rho_stream_smem(launch.variant) > 0 && (n * sizeof(float2)) % 16 == 0 &&
+            !(rs && rs[0] == '0')) {
+            d.twp_inv = upload(rho_stream_inv_twiddles(launch.variant));
+            launch.rho_stream = 1;
+        }
+        if (launch.smem * launch.per_block > 227 * 1024 ||
+            (staged_row && launch.smem + size_t(n) * sizeof(float2) > 227 * 1024))
             throw std::invalid_argument("fft: transform does not fit in shared memory");
     }
 
@@ -272,7 +283,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     g.fir = p->upload(fir);
 
     p->build_desc(g.Lf, p->d_fine, p->l_fine);
-    p->build_desc(G.n_rho, p->d_rho, p->l_rho);
+    p->build_desc(G.n_rho, p->d_rho, p->l_rho, true);
     p->build_desc(g.L2, p->d_coarse, p->l_coarse);
     p->build_desc(2L * G.N, p->d_filt, p->l_filt);
 

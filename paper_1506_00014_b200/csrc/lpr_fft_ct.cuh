@@ -29,6 +29,14 @@ __constant__ float c_wi27[27] = {0.000000000e+00f, -2.306158707e-01f, -4.4879918
 __constant__ float c_wr32[32] = {1.000000000e+00f, 9.807852804e-01f, 9.238795325e-01f, 8.314696123e-01f, 7.071067812e-01f, 5.555702330e-01f, 3.826834324e-01f, 1.950903220e-01f, 6.123233996e-17f, -1.950903220e-01f, -3.826834324e-01f, -5.555702330e-01f, -7.071067812e-01f, -8.314696123e-01f, -9.238795325e-01f, -9.807852804e-01f, -1.000000000e+00f, -9.807852804e-01f, -9.238795325e-01f, -8.314696123e-01f, -7.071067812e-01f, -5.555702330e-01f, -3.826834324e-01f, -1.950903220e-01f, -1.836970199e-16f, 1.950903220e-01f, 3.826834324e-01f, 5.555702330e-01f, 7.071067812e-01f, 8.314696123e-01f, 9.238795325e-01f, 9.807852804e-01f};
 __constant__ float c_wi32[32] = {0.000000000e+00f, -1.950903220e-01f, -3.826834324e-01f, -5.555702330e-01f, -7.071067812e-01f, -8.314696123e-01f, -9.238795325e-01f, -9.807852804e-01f, -1.000000000e+00f, -9.807852804e-01f, -9.238795325e-01f, -8.314696123e-01f, -7.071067812e-01f, -5.555702330e-01f, -3.826834324e-01f, -1.950903220e-01f, -1.224646799e-16f, 1.950903220e-01f, 3.826834324e-01f, 5.555702330e-01f, 7.071067812e-01f, 8.314696123e-01f, 9.238795325e-01f, 9.807852804e-01f, 1.000000000e+00f, 9.807852804e-01f, 9.238795325e-01f, 8.314696123e-01f, 7.071067812e-01f, 5.555702330e-01f, 3.826834324e-01f, 1.950903220e-01f};
 
+// A twiddle-row pointer the compiler cannot hoist above the preceding barrier
+// (in persistent loops it otherwise pulls every pass's table loads to the top
+// of the row body and spills).
+__device__ __forceinline__ const float2* pinned(const float2* p) {
+    asm volatile("mov.b64 %0, %0;" : "+l"(p)::"memory");
+    return p;
+}
+
 template <int R>
 __device__ __forceinline__ float2 wr(int j);
 #define LPR_WR(R)                                                                          \
@@ -127,9 +135,10 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
         if (b < B) {
             const int k = b % NS;
             if (NS > 1) {
+                const float2* tw = pinned(twp + (OFF + k));  // one base; the r offsets fold into the loads
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
-                    const float2 w = __ldg(twp + OFF + (r - 1) * NS + k);
+                    const float2 w = __ldg(tw + (r - 1) * NS);
                     v[i][r] = INV ? cmulc(v[i][r], w) : cmul(v[i][r], w);
                 }
             }
@@ -211,6 +220,115 @@ struct CtFft {
     }
 };
 
+// ---- pieces of the streamed rho pass (k_rho_stream): forward radices
+// R1, R2, R3 and the inverse in the reversed order R3, R2, R1, so the
+// forward's last butterfly and the inverse's first (twiddle-free, NS = 1)
+// butterfly see the same R3 elements: they are fused in registers with the
+// spectral multiply between them (one shared round trip instead of three).
+
+// Forward last pass (radix R at NS = N / R) x multiplier x inverse first pass.
+template <int N, int T, int S, int R, int OFF>
+__device__ __forceinline__ void ct_mid_fused(float2* x, const float2* __restrict__ twp, const float2* ms, int tid) {
+    constexpr int B = N / R;
+    constexpr int NB = (B + T - 1) / T;
+    float2 v[NB][R];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int b = tid + i * T;
+        if (b < B) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[i][r] = x[ct_pad<S>(b + r * B)];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int b = tid + i * T;
+        if (b < B) {
+            const float2* tw = pinned(twp + (OFF + b));
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], __ldg(tw + (r - 1) * B));
+            Dft<R, false>::run(v[i]);
+            float2 u[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) u[r] = cmul(v[i][Dft<R, false>::slot(r)], ms[b + r * B]);
+            Dft<R, true>::run(u);
+            if constexpr (S == 0 && R % 2 == 0) {  // R consecutive outputs: 16-byte stores, conflict-free
+                float4* dst = reinterpret_cast<float4*>(x + R * b);
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                    const float2 a = u[Dft<R, true>::slot(r)], c = u[Dft<R, true>::slot(r + 1)];
+                    dst[r / 2] = make_float4(a.x, a.y, c.x, c.y);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) x[ct_pad<S>(R * b + r)] = u[Dft<R, true>::slot(r)];
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Inverse last pass (radix R at NS = N / R) straight from registers to a
+// global row: butterfly b writes out[b + r NS], coalesced across the warp.
+// The buffer is free for the next TMA load once this returns.
+template <int N, int T, int S, int R, int OFF>
+__device__ __forceinline__ void ct_last_to_global(const float2* x, const float2* __restrict__ twp,
+                                                  float2* __restrict__ out, int tid) {
+    constexpr int B = N / R;
+    constexpr int NB = (B + T - 1) / T;
+    float2 v[NB][R];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int b = tid + i * T;
+        if (b < B) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[i][r] = x[ct_pad<S>(b + r * B)];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int b = tid + i * T;
+        if (b < B) {
+            const float2* tw = pinned(twp + (OFF + b));
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[i][r] = cmulc(v[i][r], __ldg(tw + (r - 1) * B));
+            Dft<R, true>::run(v[i]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) out[b + r * B] = v[i][Dft<R, true>::slot(r)];
+        }
+    }
+}
+
+// Streamed rho-pass plan: length N = R1 R2 R3, T threads per row.
+template <int N, int T, int S, int R1, int R2, int R3>
+struct RhoStream {
+    static constexpr int kN = N;
+    static constexpr int kT = T;
+    static constexpr int kElems = (ct_pad<S>(N - 1) + 2) / 2 * 2;  // even: every buffer starts 16-byte aligned
+    // forward (R1, R2, R3 + fused) then inverse (R2, R1 to global); the whole
+    // per-row convolution on a buffer whose row has landed
+    __device__ __forceinline__ static void convolve(float2* x, const float2* twf, const float2* twi, const float2* ms,
+                                                    float2* out, int tid) {
+        ct_pass<N, T, S, R1, 1, 0, false>(x, twf, tid);
+        ct_pass<N, T, S, R2, R1, 0, false>(x, twf, tid);
+        ct_mid_fused<N, T, S, R3, R1 * (R2 - 1)>(x, twf, ms, tid);
+        ct_pass<N, T, S, R2, R3, 0, true>(x, twi, tid);
+        ct_last_to_global<N, T, S, R1, R3 * (R2 - 1)>(x, twi, out, tid);
+    }
+    static std::vector<float2> fwd_twiddles() {
+        std::vector<float2> t;
+        ct_twiddles<N, 1, R1, R2, R3>(t);
+        return t;
+    }
+    static std::vector<float2> inv_twiddles() {
+        std::vector<float2> t;
+        ct_twiddles<N, 1, R3, R2, R1>(t);
+        return t;
+    }
+};
+
 struct GenericFft {
     static constexpr int kN = 0;
     static constexpr int kT = 0;  // runtime: threads(d)
@@ -239,5 +357,7 @@ using Fft4374 = CtFft<4374, 192, 1, 2, 0, 27, 27, 6>;
 #endif
 using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, (LPR_FFT8192_P == 1 ? 2 : 1), 4, 16, 16, 16, 2>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
+// streamed rho pass for N_rho = 4374 (2 rows in flight per block, 2 blocks per SM)
+using Rho4374 = RhoStream<4374, 192, 0, 27, 27, 6>;
 
 }  // namespace lpr

@@ -558,6 +558,80 @@ __global__ void LPR_LB(F) k_rho_pass(const __grid_constant__ DevGeom g, const __
     for (int j = tid; j < n; j += T) row[j] = a[F::idx(j)];
 }
 
+// ---- TMA bulk copies (cp.async.bulk, non-tensor) and mbarriers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// global -> shared, completion counted on bar (bytes % 16 == 0, both ends 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Streamed rho pass (the 7-smooth hot length): a block takes the rows of two
+// items at one k_theta. Both rows and their shared multiplier row are
+// requested at once by TMA bulk copy into shared memory, so the second row
+// lands while the first is transformed; the forward last / inverse first
+// butterflies are fused around the multiply and the inverse's last pass
+// stores straight from registers to the row in HBM. (Straight-line on
+// purpose: in a persistent row loop ptxas keeps every pass's loop-invariant
+// state live and spills.)
+template <class F>
+__global__ void __launch_bounds__(F::kT, 2) k_rho_stream(const __grid_constant__ DevGeom g, const float2* __restrict__ twf,
+                                                         const float2* __restrict__ twi, const float2* __restrict__ mult,
+                                                         float2* __restrict__ spec, int items) {
+    extern __shared__ __align__(16) float2 sm[];
+    __shared__ __align__(8) uint64_t bars[2];
+    constexpr int E = F::kElems;
+    const int tid = threadIdx.x;
+    const int n = g.n_rho, ks = g.nts + 1;
+    const int pairs = (items + 1) / 2;
+    const int k = blockIdx.x / pairs, i0 = 2 * (blockIdx.x % pairs);
+    const bool two = i0 + 1 < items;
+    float2* ms = sm + 2 * E;
+    const uint32_t row_bytes = uint32_t(n) * sizeof(float2);
+    float2* row0 = spec + (size_t(i0) * ks + k) * n;
+    float2* row1 = row0 + size_t(ks) * n;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&bars[0], 2 * row_bytes);
+        bulk_g2s(ms, mult + size_t(k) * n, row_bytes, &bars[0]);
+        bulk_g2s(sm, row0, row_bytes, &bars[0]);
+        if (two) {
+            mbar_expect_tx(&bars[1], row_bytes);
+            bulk_g2s(sm + E, row1, row_bytes, &bars[1]);
+        }
+    }
+    __syncthreads();
+    mbar_wait(&bars[0], 0);
+    F::convolve(sm, twf, twi, ms, row0, tid);
+    if (two) {
+        mbar_wait(&bars[1], 0);
+        F::convolve(sm + E, twf, twi, ms, row1, tid);
+    }
+}
+
 // Hermitian theta inverse: two real columns per complex transform of length
 // 2 nts; rows [j0, j0 + win) of the periodic result are kept.
 template <class F>
@@ -937,6 +1011,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
     SET((k_radon_theta_fwd<F, true>), fine.smem * fine.per_block); \
     SET(k_theta_inv_fine_T<F>, fine.smem * fine.per_block)
 #define RHO(F) SET(k_rho_pass<F>, rho.smem + rho_mult_bytes)
+    if (rho.variant == kFft4374) SET(k_rho_stream<Rho4374>, rho_stream_smem(kFft4374));
 #define COARSE(F)                                          \
     SET(k_theta_inv<F>, coarse.smem * coarse.per_block);    \
     SET(k_bp_theta_fwd<F>, coarse.smem * coarse.per_block); \
@@ -964,8 +1039,24 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
 #undef CALL
 }
 
+size_t rho_stream_smem(int variant) {
+    return variant == kFft4374 ? size_t(3) * Rho4374::kElems * sizeof(float2) : 0;
+}
+
+std::vector<float2> rho_stream_inv_twiddles(int variant) {
+    return variant == kFft4374 ? Rho4374::inv_twiddles() : std::vector<float2>{};
+}
+
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec) {
+    if (L.rho_stream && fd.twp_inv != nullptr) {
+        const int items = int(grid.y);
+        if (L.variant == kFft4374) {
+            k_rho_stream<Rho4374><<<int(grid.x) * ((items + 1) / 2), Rho4374::kT, rho_stream_smem(kFft4374), st>>>(g, fd.twp, fd.twp_inv,
+                                                                                                mult, spec, items);
+            return;
+        }
+    }
 #define CALL(F) k_rho_pass<F><<<grid, L.tpt, L.smem + size_t(g.n_rho) * sizeof(float2), st>>>(g, fd, mult, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL

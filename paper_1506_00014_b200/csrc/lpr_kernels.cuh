@@ -57,6 +57,7 @@ struct FftLaunch {
     int tpt;       // threads per transform (block size of the rho pass)
     int per_block; // transforms (column pairs) per theta block
     size_t smem;   // shared bytes of one transform
+    int rho_stream = 0;  // rho pass: 1 = the TMA-streamed two-rows-per-block kernel (k_rho_stream)
 };
 
 // host-side launchers (lpr_kernels.cu)
@@ -67,6 +68,8 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                             const Tap* qf, float2* spec, bool tex);
 void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out);
+size_t rho_stream_smem(int variant);  // 0: no streamed rho kernel for this length
+std::vector<float2> rho_stream_inv_twiddles(int variant);
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec);
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,

@@ -236,9 +236,48 @@ def test_texture_gather_ablation(lp, lpo, cuda):
         lp.radon_transpose(torch.zeros(g.n_theta, N, device=cuda), tex)
 
 
-def test_config5_n4096(lp, lpo, cuda):
+def _gaussian_case(N, n_theta):
+    """An off-centre Gaussian blob, its analytic line integrals and its
+    analytic back-projection R# R f (x) = 2 int_0^pi Rf(theta, x.theta) dtheta
+    = 2 sigma sqrt(2 pi) pi e^-a I0(a), a = |x - x0|^2 / (4 sigma^2).
+    Convention: s = x1 cos(theta) + x2 sin(theta), x1 along columns."""
+    from scipy.special import i0e
+
+    x = (np.arange(N) - N / 2) / N
+    X1, X2 = np.meshgrid(x, x)
+    x0, sig = (0.1, -0.05), 0.05
+    f = np.exp(-((X1 - x0[0]) ** 2 + (X2 - x0[1]) ** 2) / (2 * sig ** 2))
+    th = np.arange(n_theta) * np.pi / n_theta
+    proj = x0[0] * np.cos(th) + x0[1] * np.sin(th)
+    g = sig * np.sqrt(2 * np.pi) * np.exp(-(x[None, :] - proj[:, None]) ** 2 / (2 * sig ** 2))
+    a = ((X1 - x0[0]) ** 2 + (X2 - x0[1]) ** 2) / (4 * sig ** 2)
+    bp = 2 * sig * np.sqrt(2 * np.pi) * np.pi * i0e(a)
+    inside = X1 ** 2 + X2 ** 2 <= 0.25
+    return f, g, bp, inside
+
+
+@pytest.mark.parametrize("N", [2048, 4096])
+def test_gaussian_analytic(lp, lpo, cuda, N):
+    """R and R# of a smooth Gaussian against their closed forms at the bench
+    size and at config 5 (N=4096, 6144 angles): the discretisation error of
+    the method is ~1e-6 here (oracle at N=128: 2e-6), so this pins the fp32
+    GPU path at full size to the 1e-4 bar without a CPU run."""
+    import torch
+
+    g = lp.sampling_plan(N, 3, 0, lp.smooth_n_rho(N))
+    assert g.n_theta == 3 * N // 2
+    plan = lp.RadonPlan(g, max_batch=1)
+    f, sino, bp, inside = _gaussian_case(N, g.n_theta)
+    s = lp.fast_radon(torch.tensor(f, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    assert lpo.rel_l2(s, sino) <= TOL
+    b = lp.fast_backprojection(torch.tensor(sino, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    assert lpo.rel_l2(b[inside], bp[inside]) <= TOL
+    assert np.abs(b[~inside]).max() == 0.0
+
+
+def test_config5_n4096_disc(lp, lpo, cuda):
     """Config 5 (N=4096, 6144 angles): R of a centred disc is rotation
-    invariant and matches 2 sqrt(r^2 - s^2); R# R keeps the disc's symmetry."""
+    invariant and matches 2 sqrt(r^2 - s^2)."""
     import torch
 
     N = 4096
@@ -252,9 +291,6 @@ def test_config5_n4096(lp, lpo, cuda):
     want = 2 * np.sqrt(np.clip(0.04 - x ** 2, 0, None))
     assert lpo.rel_l2(s.mean(axis=0), want) <= 5e-3
     assert np.abs(s - s.mean(axis=0)).max() <= 1e-2 * want.max()
-    b = lp.fast_backprojection(torch.tensor(s, dtype=torch.float32, device=cuda), plan).cpu().numpy()
-    assert np.isfinite(b).all()
-    assert lpo.rel_l2(b, b[::-1, ::-1]) <= 1e-2  # point symmetry of a centred disc (up to the raster offset)
 
 
 def test_fbp_reconstructs_phantom(lp, lpo, cuda):
