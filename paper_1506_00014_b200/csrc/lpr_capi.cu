@@ -19,9 +19,7 @@
 namespace lpr {
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
-__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* img, Tap* q4);
 __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const float* sino, float* qg);
-__global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* sino, float* qg);
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
 __global__ void k_bp_out(DevGeom g, const float* lp, float* img);
 __global__ void k_radon_out_T(DevGeom g, const float* sino, float* lp);
@@ -132,6 +130,7 @@ struct lpr_gpu_plan {
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     bool tex_gather = false;      // LPR_PLAN_TEXTURE_GATHER ablation
+    int tex_mode = 0;             // gather path of the R fine grid: 0 quad taps, 1 hw bilinear, 2 tld4 exact taps
     cudaTextureObject_t qtex = 0;
     std::vector<void*> allocs;
     long long launches = 0, ffts = 0;
@@ -411,7 +410,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     ck(prepare_filter_kernel(p->l_filt), "filter smem attribute");
     ck(prepare_fft_kernels(p->l_fine, p->l_rho, p->l_coarse, size_t(G.n_rho) * sizeof(float2)),
        "fft smem attributes");
-    if (p->tex_gather) {
+    if (p->tex_mode) {
         // the plain coefficient rasters of the whole batch as one tall pitched
         // 2-D texture with hardware bilinear filtering
         int align = 0;
@@ -428,7 +427,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         rd.res.pitch2D.pitchInBytes = pitch_bytes;
         cudaTextureDesc td{};
         td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
-        td.filterMode = cudaFilterModeLinear;
+        td.filterMode = p->tex_mode == 1 ? cudaFilterModeLinear : cudaFilterModePoint;
         td.readMode = cudaReadModeElementType;
         td.normalizedCoords = 0;
         ck(cudaCreateTextureObject(&p->qtex, &rd, &td, nullptr), "cudaCreateTextureObject");
@@ -448,9 +447,9 @@ inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
 void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
     mark(p, 0, st);
-    launch_prefilter_2d(!p->tex_gather, nb, st, g, img, p->q4);
+    launch_prefilter_2d(p->tex_mode == 0, nb, st, g, img, p->q4);
     mark(p, 1, st);
-    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->q4, p->spec, p->tex_gather);
+    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->q4, p->spec, p->tex_mode);
     mark(p, 2, st);
     launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_R, p->spec);
     mark(p, 3, st);
@@ -637,6 +636,9 @@ int lpr_gpu_plan_create_ex(int device, const lpr_geometry* geom, const double* z
         p->geo = G;
         p->max_batch = max_batch;
         p->tex_gather = (flags & LPR_PLAN_TEXTURE_GATHER) != 0;
+        // LPR_TEX_TAPS=1: exact-tap tld4 texture gather (experiment; same numerics as the quad taps)
+        const char* tt = std::getenv("LPR_TEX_TAPS");
+        p->tex_mode = p->tex_gather ? 1 : (tt && tt[0] == '1' ? 2 : 0);
         try {
             init_plan(p, zeta, zeta_bp);
         } catch (...) {

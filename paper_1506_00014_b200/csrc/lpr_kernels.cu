@@ -54,65 +54,6 @@ __device__ __forceinline__ void bsw(float a, float w[4]) {
 // is a 33-tap separable FIR on the mirror-extended line: every output is
 // independent, so lines need no sequential scan and both passes coalesce.
 
-// Because h is symmetric, the mirrored apron coefficient at x < 0 equals the
-// FIR over the virtually extended line, sum_d h_d f(mirror(x + d)), so one
-// 2-D tile kernel produces the apron-extended coefficient raster directly:
-// a (32 + 32)^2 input tile is staged in shared memory through the mirror
-// map, filtered along rows, then along columns (reference order: rows then
-// columns, bspline.cpp:120-129).
-constexpr int kPT = 32;                      // output tile edge (rows; quad origins per row)
-constexpr int kPX = kPT + 3;                 // coefficient columns per tile row (quad = 4 taps)
-constexpr int kPEY = kPT + 2 * kFirHalf;     // staged input rows
-constexpr int kPEX = kPX + 2 * kFirHalf;     // staged input columns
-
-// Output: the quad-tap raster q4[r][c] = (Q[r][c], Q[r][c+1], Q[r][c+2], Q[r][c+3])
-// over the apron-extended grid, so every spline tap row of the fine-grid
-// gather is one 16-byte load (4 loads per sample instead of 16).
-__global__ void __launch_bounds__(256) k_prefilter_2d(DevGeom g, const float* __restrict__ img, Tap* __restrict__ q4) {
-    __shared__ float h[2 * kFirHalf + 1];
-    __shared__ float in[kPEY][kPEX + 1];
-    __shared__ float mid[kPEY][kPX + 1];
-    __shared__ float fin[kPT][kPX + 1];
-    const int tid = threadIdx.x;
-    const int N = g.N, pitch = g.pitch;
-    const int x0 = blockIdx.x * kPT, y0 = blockIdx.y * kPT, b = blockIdx.z;
-    if (tid < 2 * kFirHalf + 1) h[tid] = __ldg(g.fir + tid);
-    const float* src = img + size_t(b) * N * N;
-    const int vx0 = x0 - kApron - kFirHalf, vy0 = y0 - kApron - kFirHalf;
-    for (int idx = tid; idx < kPEY * kPEX; idx += 256) {
-        const int i = idx / kPEX, j = idx % kPEX;
-        in[i][j] = __ldg(src + size_t(mirror_idx(vy0 + i, N)) * N + mirror_idx(vx0 + j, N));
-    }
-    __syncthreads();
-    for (int idx = tid; idx < kPEY * kPX; idx += 256) {
-        const int i = idx / kPX, j = idx % kPX;
-        float acc = 0.f;
-#pragma unroll
-        for (int d = 0; d <= 2 * kFirHalf; ++d) acc = fmaf(h[d], in[i][j + d], acc);
-        mid[i][j] = acc;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < kPT * kPX; idx += 256) {
-        const int i = idx / kPX, j = idx % kPX;
-        float acc = 0.f;
-#pragma unroll
-        for (int d = 0; d <= 2 * kFirHalf; ++d) acc = fmaf(h[d], mid[i + d][j], acc);
-        fin[i][j] = acc;
-    }
-    __syncthreads();
-    Tap* dst = q4 + size_t(b) * pitch * pitch;
-    for (int idx = tid; idx < kPT * kPT; idx += 256) {
-        const int i = idx / kPT, j = idx % kPT;
-        if (y0 + i < pitch && x0 + j < pitch) {
-#if LPR_TAPS == 4
-            dst[size_t(y0 + i) * pitch + x0 + j] = make_float4(fin[i][j], fin[i][j + 1], fin[i][j + 2], fin[i][j + 3]);
-#else
-            dst[size_t(y0 + i) * pitch + x0 + j] = fin[i][j];
-#endif
-        }
-    }
-}
-
 // Recursive form of the same prefilter, for the R path: a 64 x 64 output
 // tile is staged with a 16-sample warm-up margin per side (through the
 // mirror map), then each thread runs the causal + anticausal recursion
@@ -166,7 +107,10 @@ __global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float
         const int i = idx / kIT, j = idx % kIT;
         if (y0 + i >= pitch || x0 + j >= pitch) continue;
         const float* r = s[kIW + i] + kIW + j;
-        if constexpr (sizeof(T) == sizeof(float4)) {
+        if constexpr (sizeof(T) == 2 * sizeof(float4)) {  // octo: this row's quad and the next row's
+            const float* r2 = r + kICP;
+            dst[size_t(y0 + i) * pitch + x0 + j] = T{make_float4(r[0], r[1], r[2], r[3]), make_float4(r2[0], r2[1], r2[2], r2[3])};
+        } else if constexpr (sizeof(T) == sizeof(float4)) {
             dst[size_t(y0 + i) * pitch + x0 + j] = make_float4(r[0], r[1], r[2], r[3]);
         } else {
             dst[size_t(y0 + i) * pitch + x0 + j] = r[0];
@@ -216,25 +160,6 @@ __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const flo
         const int i = idx / kSCols, j = idx % kSCols;
         if (c0col + j < N) qg[(size_t(b) * g.n_theta + i0 + i) * N + c0col + j] = s[i][kIW + j];
     }
-}
-
-// sinogram rows (R#, Alg. 2 step 1): prefilter along s only.
-__global__ void __launch_bounds__(256) k_prefilter_sino(DevGeom g, const float* __restrict__ sino, float* __restrict__ qg) {
-    __shared__ float h[2 * kFirHalf + 1];
-    __shared__ float in[256 + 2 * kFirHalf];
-    const int tid = threadIdx.x;
-    const int c0 = blockIdx.x * 256, i = blockIdx.y, b = blockIdx.z;
-    const int N = g.N;
-    if (tid < 2 * kFirHalf + 1) h[tid] = __ldg(g.fir + tid);
-    const float* src = sino + (size_t(b) * g.n_theta + i) * N;
-    for (int j = tid; j < 256 + 2 * kFirHalf; j += 256) in[j] = __ldg(src + mirror_idx(c0 - kFirHalf + j, N));
-    __syncthreads();
-    const int c = c0 + tid;
-    if (c >= N) return;
-    float acc = 0.f;
-#pragma unroll
-    for (int d = 0; d <= 2 * kFirHalf; ++d) acc = fmaf(h[d], in[tid + d], acc);
-    qg[(size_t(b) * g.n_theta + i) * N + c] = acc;
 }
 
 // ------------------------------------------------------------- FFT-policy kernels
@@ -378,6 +303,15 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
     return true;
 }
 
+#if LPR_TAPS == 8
+// One 32-byte read-only load (LDG.256, sm_100): two tap rows of 4 coefficients.
+__device__ __forceinline__ void ldg_octo(const Octo* p, float4& a, float4& b) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+}
+#endif
+
 __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __restrict__ q4, const FineRow& r,
                                               float vc, float vr, float er) {
     float tc, tr;
@@ -388,6 +322,14 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __res
     bsw(tr - kr, wr);
     const Tap* p = q4 + (int(kr) - 1 + kApron) * g.pitch + (int(kc) - 1 + kApron);
     float acc = 0.f;
+#if LPR_TAPS == 8
+    float4 t[4];
+    ldg_octo(p, t[0], t[1]);                // tap rows kr-1, kr
+    ldg_octo(p + 2 * g.pitch, t[2], t[3]);  // tap rows kr+1, kr+2
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+        acc = fmaf(wr[a], fmaf(wc[0], t[a].x, fmaf(wc[1], t[a].y, fmaf(wc[2], t[a].z, wc[3] * t[a].w))), acc);
+#else
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
 #if LPR_TAPS == 4
@@ -398,6 +340,7 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __res
 #endif
         acc = fmaf(wr[a], fmaf(wc[0], t.x, fmaf(wc[1], t.y, fmaf(wc[2], t.z, wc[3] * t.w))), acc);
     }
+#endif
     return er * acc;
 }
 
@@ -462,18 +405,47 @@ __device__ __forceinline__ float gather_tex(const DevGeom& g, const FineRow& r, 
     return er * fmaf(gr0, top, gr1 * bot);
 }
 
+// Exact-tap texture variant: the 4 x 4 spline footprint as four tld4
+// gathers (2 x 2 texels each, returned unfiltered in fp32) from the plain
+// coefficient raster, weights in fp32 as in gather_image. The texture path
+// brings the 2-D block-linear cache layout and its own fetch pipeline.
+__device__ __forceinline__ float gather_tld4(const DevGeom& g, const FineRow& r, float vc, float vr, float er, int b) {
+    float tc, tr;
+    if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
+    const float kc = floorf(tc), kr = floorf(tr);
+    float wc[4], wr[4];
+    bsw(tc - kc, wc);
+    bsw(tr - kr, wr);
+    // tld4 at (x, y) returns texels (x0, y1), (x1, y1), (x1, y0), (x0, y0) with x0 = floor(x - 1/2)
+    const float x0 = kc + float(kApron), x1 = x0 + 2.f;  // columns kc-1, kc | kc+1, kc+2
+    const float yb = float(b * g.pitch) + kr + float(kApron);
+    const float4 a = tex2Dgather<float4>(g.qtex, x0, yb, 0);        // rows kr-1, kr
+    const float4 c = tex2Dgather<float4>(g.qtex, x1, yb, 0);
+    const float4 d = tex2Dgather<float4>(g.qtex, x0, yb + 2.f, 0);  // rows kr+1, kr+2
+    const float4 e = tex2Dgather<float4>(g.qtex, x1, yb + 2.f, 0);
+    const float r0 = fmaf(wc[0], a.w, fmaf(wc[1], a.z, fmaf(wc[2], c.w, wc[3] * c.z)));
+    const float r1 = fmaf(wc[0], a.x, fmaf(wc[1], a.y, fmaf(wc[2], c.x, wc[3] * c.y)));
+    const float r2 = fmaf(wc[0], d.w, fmaf(wc[1], d.z, fmaf(wc[2], e.w, wc[3] * e.z)));
+    const float r3 = fmaf(wc[0], d.x, fmaf(wc[1], d.y, fmaf(wc[2], e.x, wc[3] * e.y)));
+    return er * fmaf(wr[0], r0, fmaf(wr[1], r1, fmaf(wr[2], r2, wr[3] * r3)));
+}
+
 // Alg. 1 steps 3-6a: gather T_m f e^rho on the fine grid of two rho columns,
 // zero-embed into the doubled fine period Lf, real theta FFT, keep |k| < nts.
 // Each thread gathers two fine rows per iteration (64 independent tap loads
 // in flight) to hide the L2 latency of the spline taps.
-template <class F, bool TEX = false>
+template <class F, int TEX = 0>
 __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                             const Tap* __restrict__ qf, float2* __restrict__ spec) {
     extern __shared__ float2 smem[];
     const Group<F> G;
     const int E = F::elems(fd);
     float2* sm = smem + G.g * E;
+#ifdef LPR_FORCE_SECTOR  // timing experiment only: every block gathers sector LPR_FORCE_SECTOR
+    const int m = LPR_FORCE_SECTOR, b = blockIdx.z;
+#else
     const int m = blockIdx.y, b = blockIdx.z;
+#endif
     const int l0b = 2 * F::kP * blockIdx.x, l0 = l0b + 2 * G.g;
     const int Lf = g.Lf, nf = g.nf;
     const Tap* q = qf + size_t(b) * g.pitch * g.pitch;
@@ -484,15 +456,23 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
     if constexpr (kFusedFirstPass<F>) {
         if (F::kN == Lf) {
             first_pass_gathered<F>(sm, G.tid, [&](int row) {
+#ifdef LPR_EXP_NOGATHER  // timing experiment only: no image taps
+                return make_float2(er0 * row, er1 * row);
+#endif
                 const FineRow fr = fine_row(g, cm, smm, __ldg(g.fine_cos + row), __ldg(g.fine_sin + row));
-                if constexpr (TEX)
+                if constexpr (TEX == 1)
                     return make_float2(one ? gather_tex(g, fr, vc, vr, er0, b) : 0.f,
                                        two ? gather_tex(g, fr, vc, vr, er1, b) : 0.f);
+                else if constexpr (TEX == 2)
+                    return make_float2(one ? gather_tld4(g, fr, vc, vr, er0, b) : 0.f,
+                                       two ? gather_tld4(g, fr, vc, vr, er1, b) : 0.f);
                 else
                     return make_float2(one ? gather_image(g, q, fr, vc, vr, er0) : 0.f,
                                        two ? gather_image(g, q, fr, vc, vr, er1) : 0.f);
             });
+#ifndef LPR_EXP_NOFFT  // timing experiment only: skip the FFT passes after the gathered first pass
             F::template run_tail<false>(sm, fd, G.tid);
+#endif
             float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
             store_half_spectra<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out);
             return;
@@ -508,7 +488,12 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         const FineRow r1 = fine_row(g, cm, smm, __ldg(g.fine_cos + i), __ldg(g.fine_sin + i));
         const FineRow r2 = fine_row(g, cm, smm, __ldg(g.fine_cos + i2), __ldg(g.fine_sin + i2));
         float h0, h1, h2, h3;
-        if constexpr (TEX) {
+        if constexpr (TEX == 2) {
+            h0 = one ? gather_tld4(g, r1, vc, vr, er0, b) : 0.f;
+            h1 = two ? gather_tld4(g, r1, vc, vr, er1, b) : 0.f;
+            h2 = one ? gather_tld4(g, r2, vc, vr, er0, b) : 0.f;
+            h3 = two ? gather_tld4(g, r2, vc, vr, er1, b) : 0.f;
+        } else if constexpr (TEX == 1) {
             h0 = one ? gather_tex(g, r1, vc, vr, er0, b) : 0.f;
             h1 = two ? gather_tex(g, r1, vc, vr, er1, b) : 0.f;
             h2 = one ? gather_tex(g, r2, vc, vr, er0, b) : 0.f;
@@ -1008,7 +993,8 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
     } while (0)
 #define FINE(F)                                                   \
     SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block);         \
-    SET((k_radon_theta_fwd<F, true>), fine.smem * fine.per_block); \
+    SET((k_radon_theta_fwd<F, 1>), fine.smem * fine.per_block);    \
+    SET((k_radon_theta_fwd<F, 2>), fine.smem * fine.per_block);    \
     SET(k_theta_inv_fine_T<F>, fine.smem * fine.per_block)
 #define RHO(F) SET(k_rho_pass<F>, rho.smem + rho_mult_bytes)
     if (rho.variant == kFft4374) SET(k_rho_stream<Rho4374>, rho_stream_smem(kFft4374));
@@ -1027,9 +1013,15 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 }
 
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const Tap* qf, float2* spec, bool tex) {
-    if (tex) {
-#define CALL(F) k_radon_theta_fwd<F, true><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
+                            const Tap* qf, float2* spec, int tex) {
+    if (tex == 1) {
+#define CALL(F) k_radon_theta_fwd<F, 1><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
+        LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+        return;
+    }
+    if (tex == 2) {
+#define CALL(F) k_radon_theta_fwd<F, 2><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
         LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
         return;

@@ -13,12 +13,18 @@ namespace lpr {
 constexpr int kMaxSectors = 16;
 
 // Layout of the image B-spline coefficients read by the fine-grid gather:
-// LPR_TAPS 4 = quad-tap float4 rows (4 consecutive coefficients per element,
-// one 16-byte load per tap row), 1 = plain fp32 raster (4 loads per tap row).
+// LPR_TAPS 8 = octo taps (element [r][c] = Q[r][c..c+3] and Q[r+1][c..c+3],
+// 32 bytes: two spline tap rows per LDG.256, so a sample is 2 loads),
+// 4 = quad taps (one 16-byte load per tap row), 1 = plain fp32 raster.
 #ifndef LPR_TAPS
-#define LPR_TAPS 4
+#define LPR_TAPS 8
 #endif
-#if LPR_TAPS == 4
+struct __align__(32) Octo {
+    float4 lo, hi;
+};
+#if LPR_TAPS == 8
+using Tap = Octo;
+#elif LPR_TAPS == 4
 using Tap = float4;
 #else
 using Tap = float;
@@ -66,7 +72,7 @@ std::vector<float2> fft_pass_twiddles(int variant);
 cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
                                 size_t rho_mult_bytes);
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const Tap* qf, float2* spec, bool tex);
+                            const Tap* qf, float2* spec, int tex);  // tex: 0 soft taps, 1 hw bilinear, 2 tld4 exact taps
 void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out);
 size_t rho_stream_smem(int variant);  // 0: no streamed rho kernel for this length
 std::vector<float2> rho_stream_inv_twiddles(int variant);
