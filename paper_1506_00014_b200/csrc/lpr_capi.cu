@@ -196,6 +196,7 @@ struct lpr_gpu_plan {
         const char* rs = std::getenv("LPR_RHO_STREAM");
         if (staged_row && rho_stream_smem(launch.variant) > 0 && (n * sizeof(float2)) % 16 == 0 &&
             !(rs && rs[0] == '0')) {
+            d.twp_sfwd = upload(rho_stream_fwd_twiddles(launch.variant));
             d.twp_inv = upload(rho_stream_inv_twiddles(launch.variant));
             launch.rho_stream = 1;
         }

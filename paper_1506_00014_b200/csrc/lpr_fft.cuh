@@ -25,7 +25,8 @@ struct FftDesc {
     int radix[kMaxPasses] = {};
     const float2* tw = nullptr;   // tw[j] = exp(-2 pi i j / n)
     const float2* twp = nullptr;  // per-pass twiddles of the compile-time plan (lpr_fft_ct.cuh)
-    const float2* twp_inv = nullptr;  // same for the reversed radix order (the streamed rho pass's inverse)
+    const float4* twp_sfwd = nullptr;  // streamed rho pass: forward per-pass twiddles of its radix order (tw4 form)
+    const float4* twp_inv = nullptr;   // ... and of the reversed order, conjugated (its inverse)
     // Bluestein: when nb > 0 the transform of length n runs through length nb
     int nb = 0;
     int nbpass = 0;

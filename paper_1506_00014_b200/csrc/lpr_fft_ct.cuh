@@ -10,45 +10,62 @@
 #pragma once
 
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "lpr_fft.cuh"
 
+#ifndef LPR_RHO_TW_TABLE
+#define LPR_RHO_TW_TABLE 0  // streamed rho pass: 1 = twiddle tables from global, 0 = computed (__sincosf + powers)
+#endif
+
 namespace lpr {
 
-__constant__ float c_wr6[6] = {1.000000000e+00f, 5.000000000e-01f, -5.000000000e-01f, -1.000000000e+00f, -5.000000000e-01f, 5.000000000e-01f};
-__constant__ float c_wi6[6] = {0.000000000e+00f, -8.660254038e-01f, -8.660254038e-01f, -1.224646799e-16f, 8.660254038e-01f, 8.660254038e-01f};
-__constant__ float c_wr9[9] = {1.000000000e+00f, 7.660444431e-01f, 1.736481777e-01f, -5.000000000e-01f, -9.396926208e-01f, -9.396926208e-01f, -5.000000000e-01f, 1.736481777e-01f, 7.660444431e-01f};
-__constant__ float c_wi9[9] = {0.000000000e+00f, -6.427876097e-01f, -9.848077530e-01f, -8.660254038e-01f, -3.420201433e-01f, 3.420201433e-01f, 8.660254038e-01f, 9.848077530e-01f, 6.427876097e-01f};
-__constant__ float c_wr12[12] = {1.000000000e+00f, 8.660254038e-01f, 5.000000000e-01f, 6.123233996e-17f, -5.000000000e-01f, -8.660254038e-01f, -1.000000000e+00f, -8.660254038e-01f, -5.000000000e-01f, -1.836970199e-16f, 5.000000000e-01f, 8.660254038e-01f};
-__constant__ float c_wi12[12] = {0.000000000e+00f, -5.000000000e-01f, -8.660254038e-01f, -1.000000000e+00f, -8.660254038e-01f, -5.000000000e-01f, -1.224646799e-16f, 5.000000000e-01f, 8.660254038e-01f, 1.000000000e+00f, 8.660254038e-01f, 5.000000000e-01f};
-__constant__ float c_wr16[16] = {1.000000000e+00f, 9.238795325e-01f, 7.071067812e-01f, 3.826834324e-01f, 6.123233996e-17f, -3.826834324e-01f, -7.071067812e-01f, -9.238795325e-01f, -1.000000000e+00f, -9.238795325e-01f, -7.071067812e-01f, -3.826834324e-01f, -1.836970199e-16f, 3.826834324e-01f, 7.071067812e-01f, 9.238795325e-01f};
-__constant__ float c_wi16[16] = {0.000000000e+00f, -3.826834324e-01f, -7.071067812e-01f, -9.238795325e-01f, -1.000000000e+00f, -9.238795325e-01f, -7.071067812e-01f, -3.826834324e-01f, -1.224646799e-16f, 3.826834324e-01f, 7.071067812e-01f, 9.238795325e-01f, 1.000000000e+00f, 9.238795325e-01f, 7.071067812e-01f, 3.826834324e-01f};
-__constant__ float c_wr27[27] = {1.000000000e+00f, 9.730448706e-01f, 8.936326403e-01f, 7.660444431e-01f, 5.971585917e-01f, 3.960797660e-01f, 1.736481777e-01f, -5.814482891e-02f, -2.868032327e-01f, -5.000000000e-01f, -6.862416379e-01f, -8.354878114e-01f, -9.396926208e-01f, -9.932383577e-01f, -9.932383577e-01f, -9.396926208e-01f, -8.354878114e-01f, -6.862416379e-01f, -5.000000000e-01f, -2.868032327e-01f, -5.814482891e-02f, 1.736481777e-01f, 3.960797660e-01f, 5.971585917e-01f, 7.660444431e-01f, 8.936326403e-01f, 9.730448706e-01f};
-__constant__ float c_wi27[27] = {0.000000000e+00f, -2.306158707e-01f, -4.487991802e-01f, -6.427876097e-01f, -8.021231928e-01f, -9.182161069e-01f, -9.848077530e-01f, -9.983081583e-01f, -9.579895123e-01f, -8.660254038e-01f, -7.273736416e-01f, -5.495089781e-01f, -3.420201433e-01f, -1.160929141e-01f, 1.160929141e-01f, 3.420201433e-01f, 5.495089781e-01f, 7.273736416e-01f, 8.660254038e-01f, 9.579895123e-01f, 9.983081583e-01f, 9.848077530e-01f, 9.182161069e-01f, 8.021231928e-01f, 6.427876097e-01f, 4.487991802e-01f, 2.306158707e-01f};
-__constant__ float c_wr32[32] = {1.000000000e+00f, 9.807852804e-01f, 9.238795325e-01f, 8.314696123e-01f, 7.071067812e-01f, 5.555702330e-01f, 3.826834324e-01f, 1.950903220e-01f, 6.123233996e-17f, -1.950903220e-01f, -3.826834324e-01f, -5.555702330e-01f, -7.071067812e-01f, -8.314696123e-01f, -9.238795325e-01f, -9.807852804e-01f, -1.000000000e+00f, -9.807852804e-01f, -9.238795325e-01f, -8.314696123e-01f, -7.071067812e-01f, -5.555702330e-01f, -3.826834324e-01f, -1.950903220e-01f, -1.836970199e-16f, 1.950903220e-01f, 3.826834324e-01f, 5.555702330e-01f, 7.071067812e-01f, 8.314696123e-01f, 9.238795325e-01f, 9.807852804e-01f};
-__constant__ float c_wi32[32] = {0.000000000e+00f, -1.950903220e-01f, -3.826834324e-01f, -5.555702330e-01f, -7.071067812e-01f, -8.314696123e-01f, -9.238795325e-01f, -9.807852804e-01f, -1.000000000e+00f, -9.807852804e-01f, -9.238795325e-01f, -8.314696123e-01f, -7.071067812e-01f, -5.555702330e-01f, -3.826834324e-01f, -1.950903220e-01f, -1.224646799e-16f, 1.950903220e-01f, 3.826834324e-01f, 5.555702330e-01f, 7.071067812e-01f, 8.314696123e-01f, 9.238795325e-01f, 9.807852804e-01f, 1.000000000e+00f, 9.807852804e-01f, 9.238795325e-01f, 8.314696123e-01f, 7.071067812e-01f, 5.555702330e-01f, 3.826834324e-01f, 1.950903220e-01f};
+// Radix-R roots W_R^j = (c, s) = exp(-2 pi i j / R) in the (c, s, -s, c)
+// form of tw_mul (c_wqc: the conjugate, for inverse butterflies), so a
+// constant twiddle is one FMUL2 + one FFMA2 on uniform-register pairs.
+__constant__ float4 c_wq6[6] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, 5.000000000e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-1.000000000e+00f, -1.224646799e-16f, 1.224646799e-16f, -1.000000000e+00f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, 5.000000000e-01f}};
+__constant__ float4 c_wqc6[6] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, 5.000000000e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-1.000000000e+00f, 1.224646799e-16f, -1.224646799e-16f, -1.000000000e+00f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, 5.000000000e-01f}};
+__constant__ float4 c_wq9[9] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, 7.660444431e-01f}, {1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, 1.736481777e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, -9.396926208e-01f}, {-9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, -9.396926208e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, 1.736481777e-01f}, {7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, 7.660444431e-01f}};
+__constant__ float4 c_wqc9[9] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, 7.660444431e-01f}, {1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, 1.736481777e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, -9.396926208e-01f}, {-9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, -9.396926208e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, 1.736481777e-01f}, {7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, 7.660444431e-01f}};
+__constant__ float4 c_wq12[12] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {8.660254038e-01f, -5.000000000e-01f, 5.000000000e-01f, 8.660254038e-01f}, {5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, 5.000000000e-01f}, {6.123233996e-17f, -1.000000000e+00f, 1.000000000e+00f, 6.123233996e-17f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-8.660254038e-01f, -5.000000000e-01f, 5.000000000e-01f, -8.660254038e-01f}, {-1.000000000e+00f, -1.224646799e-16f, 1.224646799e-16f, -1.000000000e+00f}, {-8.660254038e-01f, 5.000000000e-01f, -5.000000000e-01f, -8.660254038e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-1.836970199e-16f, 1.000000000e+00f, -1.000000000e+00f, -1.836970199e-16f}, {5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, 5.000000000e-01f}, {8.660254038e-01f, 5.000000000e-01f, -5.000000000e-01f, 8.660254038e-01f}};
+__constant__ float4 c_wqc12[12] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {8.660254038e-01f, 5.000000000e-01f, -5.000000000e-01f, 8.660254038e-01f}, {5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, 5.000000000e-01f}, {6.123233996e-17f, 1.000000000e+00f, -1.000000000e+00f, 6.123233996e-17f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-8.660254038e-01f, 5.000000000e-01f, -5.000000000e-01f, -8.660254038e-01f}, {-1.000000000e+00f, 1.224646799e-16f, -1.224646799e-16f, -1.000000000e+00f}, {-8.660254038e-01f, -5.000000000e-01f, 5.000000000e-01f, -8.660254038e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-1.836970199e-16f, -1.000000000e+00f, 1.000000000e+00f, -1.836970199e-16f}, {5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, 5.000000000e-01f}, {8.660254038e-01f, -5.000000000e-01f, 5.000000000e-01f, 8.660254038e-01f}};
+__constant__ float4 c_wq16[16] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, 9.238795325e-01f}, {7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, 7.071067812e-01f}, {3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, 3.826834324e-01f}, {6.123233996e-17f, -1.000000000e+00f, 1.000000000e+00f, 6.123233996e-17f}, {-3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, -3.826834324e-01f}, {-7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f}, {-9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, -9.238795325e-01f}, {-1.000000000e+00f, -1.224646799e-16f, 1.224646799e-16f, -1.000000000e+00f}, {-9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, -9.238795325e-01f}, {-7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, -7.071067812e-01f}, {-3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, -3.826834324e-01f}, {-1.836970199e-16f, 1.000000000e+00f, -1.000000000e+00f, -1.836970199e-16f}, {3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, 3.826834324e-01f}, {7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f}, {9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, 9.238795325e-01f}};
+__constant__ float4 c_wqc16[16] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, 9.238795325e-01f}, {7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f}, {3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, 3.826834324e-01f}, {6.123233996e-17f, 1.000000000e+00f, -1.000000000e+00f, 6.123233996e-17f}, {-3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, -3.826834324e-01f}, {-7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, -7.071067812e-01f}, {-9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, -9.238795325e-01f}, {-1.000000000e+00f, 1.224646799e-16f, -1.224646799e-16f, -1.000000000e+00f}, {-9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, -9.238795325e-01f}, {-7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f}, {-3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, -3.826834324e-01f}, {-1.836970199e-16f, -1.000000000e+00f, 1.000000000e+00f, -1.836970199e-16f}, {3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, 3.826834324e-01f}, {7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, 7.071067812e-01f}, {9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, 9.238795325e-01f}};
+__constant__ float4 c_wq27[27] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {9.730448706e-01f, -2.306158707e-01f, 2.306158707e-01f, 9.730448706e-01f}, {8.936326403e-01f, -4.487991802e-01f, 4.487991802e-01f, 8.936326403e-01f}, {7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, 7.660444431e-01f}, {5.971585917e-01f, -8.021231928e-01f, 8.021231928e-01f, 5.971585917e-01f}, {3.960797660e-01f, -9.182161069e-01f, 9.182161069e-01f, 3.960797660e-01f}, {1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, 1.736481777e-01f}, {-5.814482891e-02f, -9.983081583e-01f, 9.983081583e-01f, -5.814482891e-02f}, {-2.868032327e-01f, -9.579895123e-01f, 9.579895123e-01f, -2.868032327e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-6.862416379e-01f, -7.273736416e-01f, 7.273736416e-01f, -6.862416379e-01f}, {-8.354878114e-01f, -5.495089781e-01f, 5.495089781e-01f, -8.354878114e-01f}, {-9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, -9.396926208e-01f}, {-9.932383577e-01f, -1.160929141e-01f, 1.160929141e-01f, -9.932383577e-01f}, {-9.932383577e-01f, 1.160929141e-01f, -1.160929141e-01f, -9.932383577e-01f}, {-9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, -9.396926208e-01f}, {-8.354878114e-01f, 5.495089781e-01f, -5.495089781e-01f, -8.354878114e-01f}, {-6.862416379e-01f, 7.273736416e-01f, -7.273736416e-01f, -6.862416379e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-2.868032327e-01f, 9.579895123e-01f, -9.579895123e-01f, -2.868032327e-01f}, {-5.814482891e-02f, 9.983081583e-01f, -9.983081583e-01f, -5.814482891e-02f}, {1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, 1.736481777e-01f}, {3.960797660e-01f, 9.182161069e-01f, -9.182161069e-01f, 3.960797660e-01f}, {5.971585917e-01f, 8.021231928e-01f, -8.021231928e-01f, 5.971585917e-01f}, {7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, 7.660444431e-01f}, {8.936326403e-01f, 4.487991802e-01f, -4.487991802e-01f, 8.936326403e-01f}, {9.730448706e-01f, 2.306158707e-01f, -2.306158707e-01f, 9.730448706e-01f}};
+__constant__ float4 c_wqc27[27] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {9.730448706e-01f, 2.306158707e-01f, -2.306158707e-01f, 9.730448706e-01f}, {8.936326403e-01f, 4.487991802e-01f, -4.487991802e-01f, 8.936326403e-01f}, {7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, 7.660444431e-01f}, {5.971585917e-01f, 8.021231928e-01f, -8.021231928e-01f, 5.971585917e-01f}, {3.960797660e-01f, 9.182161069e-01f, -9.182161069e-01f, 3.960797660e-01f}, {1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, 1.736481777e-01f}, {-5.814482891e-02f, 9.983081583e-01f, -9.983081583e-01f, -5.814482891e-02f}, {-2.868032327e-01f, 9.579895123e-01f, -9.579895123e-01f, -2.868032327e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-6.862416379e-01f, 7.273736416e-01f, -7.273736416e-01f, -6.862416379e-01f}, {-8.354878114e-01f, 5.495089781e-01f, -5.495089781e-01f, -8.354878114e-01f}, {-9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, -9.396926208e-01f}, {-9.932383577e-01f, 1.160929141e-01f, -1.160929141e-01f, -9.932383577e-01f}, {-9.932383577e-01f, -1.160929141e-01f, 1.160929141e-01f, -9.932383577e-01f}, {-9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, -9.396926208e-01f}, {-8.354878114e-01f, -5.495089781e-01f, 5.495089781e-01f, -8.354878114e-01f}, {-6.862416379e-01f, -7.273736416e-01f, 7.273736416e-01f, -6.862416379e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-2.868032327e-01f, -9.579895123e-01f, 9.579895123e-01f, -2.868032327e-01f}, {-5.814482891e-02f, -9.983081583e-01f, 9.983081583e-01f, -5.814482891e-02f}, {1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, 1.736481777e-01f}, {3.960797660e-01f, -9.182161069e-01f, 9.182161069e-01f, 3.960797660e-01f}, {5.971585917e-01f, -8.021231928e-01f, 8.021231928e-01f, 5.971585917e-01f}, {7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, 7.660444431e-01f}, {8.936326403e-01f, -4.487991802e-01f, 4.487991802e-01f, 8.936326403e-01f}, {9.730448706e-01f, -2.306158707e-01f, 2.306158707e-01f, 9.730448706e-01f}};
+__constant__ float4 c_wq32[32] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {9.807852804e-01f, -1.950903220e-01f, 1.950903220e-01f, 9.807852804e-01f}, {9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, 9.238795325e-01f}, {8.314696123e-01f, -5.555702330e-01f, 5.555702330e-01f, 8.314696123e-01f}, {7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, 7.071067812e-01f}, {5.555702330e-01f, -8.314696123e-01f, 8.314696123e-01f, 5.555702330e-01f}, {3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, 3.826834324e-01f}, {1.950903220e-01f, -9.807852804e-01f, 9.807852804e-01f, 1.950903220e-01f}, {6.123233996e-17f, -1.000000000e+00f, 1.000000000e+00f, 6.123233996e-17f}, {-1.950903220e-01f, -9.807852804e-01f, 9.807852804e-01f, -1.950903220e-01f}, {-3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, -3.826834324e-01f}, {-5.555702330e-01f, -8.314696123e-01f, 8.314696123e-01f, -5.555702330e-01f}, {-7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f}, {-8.314696123e-01f, -5.555702330e-01f, 5.555702330e-01f, -8.314696123e-01f}, {-9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, -9.238795325e-01f}, {-9.807852804e-01f, -1.950903220e-01f, 1.950903220e-01f, -9.807852804e-01f}, {-1.000000000e+00f, -1.224646799e-16f, 1.224646799e-16f, -1.000000000e+00f}, {-9.807852804e-01f, 1.950903220e-01f, -1.950903220e-01f, -9.807852804e-01f}, {-9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, -9.238795325e-01f}, {-8.314696123e-01f, 5.555702330e-01f, -5.555702330e-01f, -8.314696123e-01f}, {-7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, -7.071067812e-01f}, {-5.555702330e-01f, 8.314696123e-01f, -8.314696123e-01f, -5.555702330e-01f}, {-3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, -3.826834324e-01f}, {-1.950903220e-01f, 9.807852804e-01f, -9.807852804e-01f, -1.950903220e-01f}, {-1.836970199e-16f, 1.000000000e+00f, -1.000000000e+00f, -1.836970199e-16f}, {1.950903220e-01f, 9.807852804e-01f, -9.807852804e-01f, 1.950903220e-01f}, {3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, 3.826834324e-01f}, {5.555702330e-01f, 8.314696123e-01f, -8.314696123e-01f, 5.555702330e-01f}, {7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f}, {8.314696123e-01f, 5.555702330e-01f, -5.555702330e-01f, 8.314696123e-01f}, {9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, 9.238795325e-01f}, {9.807852804e-01f, 1.950903220e-01f, -1.950903220e-01f, 9.807852804e-01f}};
+__constant__ float4 c_wqc32[32] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {9.807852804e-01f, 1.950903220e-01f, -1.950903220e-01f, 9.807852804e-01f}, {9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, 9.238795325e-01f}, {8.314696123e-01f, 5.555702330e-01f, -5.555702330e-01f, 8.314696123e-01f}, {7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f}, {5.555702330e-01f, 8.314696123e-01f, -8.314696123e-01f, 5.555702330e-01f}, {3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, 3.826834324e-01f}, {1.950903220e-01f, 9.807852804e-01f, -9.807852804e-01f, 1.950903220e-01f}, {6.123233996e-17f, 1.000000000e+00f, -1.000000000e+00f, 6.123233996e-17f}, {-1.950903220e-01f, 9.807852804e-01f, -9.807852804e-01f, -1.950903220e-01f}, {-3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, -3.826834324e-01f}, {-5.555702330e-01f, 8.314696123e-01f, -8.314696123e-01f, -5.555702330e-01f}, {-7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, -7.071067812e-01f}, {-8.314696123e-01f, 5.555702330e-01f, -5.555702330e-01f, -8.314696123e-01f}, {-9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, -9.238795325e-01f}, {-9.807852804e-01f, 1.950903220e-01f, -1.950903220e-01f, -9.807852804e-01f}, {-1.000000000e+00f, 1.224646799e-16f, -1.224646799e-16f, -1.000000000e+00f}, {-9.807852804e-01f, -1.950903220e-01f, 1.950903220e-01f, -9.807852804e-01f}, {-9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, -9.238795325e-01f}, {-8.314696123e-01f, -5.555702330e-01f, 5.555702330e-01f, -8.314696123e-01f}, {-7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f}, {-5.555702330e-01f, -8.314696123e-01f, 8.314696123e-01f, -5.555702330e-01f}, {-3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, -3.826834324e-01f}, {-1.950903220e-01f, -9.807852804e-01f, 9.807852804e-01f, -1.950903220e-01f}, {-1.836970199e-16f, -1.000000000e+00f, 1.000000000e+00f, -1.836970199e-16f}, {1.950903220e-01f, -9.807852804e-01f, 9.807852804e-01f, 1.950903220e-01f}, {3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, 3.826834324e-01f}, {5.555702330e-01f, -8.314696123e-01f, 8.314696123e-01f, 5.555702330e-01f}, {7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, 7.071067812e-01f}, {8.314696123e-01f, -5.555702330e-01f, 5.555702330e-01f, 8.314696123e-01f}, {9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, 9.238795325e-01f}, {9.807852804e-01f, -1.950903220e-01f, 1.950903220e-01f, 9.807852804e-01f}};
+
 
 // A twiddle-row pointer the compiler cannot hoist above the preceding barrier
 // (in persistent loops it otherwise pulls every pass's table loads to the top
 // of the row body and spills).
-__device__ __forceinline__ const float2* pinned(const float2* p) {
+template <class P>
+__device__ __forceinline__ const P* pinned(const P* p) {
     asm volatile("mov.b64 %0, %0;" : "+l"(p)::"memory");
     return p;
 }
 
-template <int R>
-__device__ __forceinline__ float2 wr(int j);
-#define LPR_WR(R)                                                                          \
-    template <>                                                                            \
-    __device__ __forceinline__ float2 wr<R>(int j) { return make_float2(c_wr##R[j], c_wi##R[j]); }
-LPR_WR(6)
-LPR_WR(9)
-LPR_WR(12)
-LPR_WR(16)
-LPR_WR(27)
-LPR_WR(32)
-#undef LPR_WR
+template <int R, bool INV>
+__device__ __forceinline__ float4 wq(int j);
+#define LPR_WQ(R)                                                                                          \
+    template <>                                                                                            \
+    __device__ __forceinline__ float4 wq<R, false>(int j) { return c_wq##R[j]; }                            \
+    template <>                                                                                            \
+    __device__ __forceinline__ float4 wq<R, true>(int j) { return c_wqc##R[j]; }
+LPR_WQ(6)
+LPR_WQ(9)
+LPR_WQ(12)
+LPR_WQ(16)
+LPR_WQ(27)
+LPR_WQ(32)
+#undef LPR_WQ
+
+// a * w for a (c, s, -s, c) entry
+__device__ __forceinline__ float2 cmul_q(float2 a, float4 w) {
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(w.z, w.w), __fmul2_rn(make_float2(a.x, a.x), make_float2(w.x, w.y)));
+}
 
 // Composite radix R = P * Q in registers, natural order in and out:
 // x[Q n1 + n2] -> P-point DFTs over n1, twiddle W_R^{n2 k1}, Q-point DFTs over n2
@@ -70,8 +87,7 @@ __device__ __forceinline__ void dft_pq(float2* v) {
     for (int k1 = 1; k1 < P; ++k1)
 #pragma unroll
         for (int n2 = 1; n2 < Q; ++n2) {
-            const float2 w = wr<R>((n2 * k1) % R);
-            v[Q * k1 + n2] = INV ? cmulc(v[Q * k1 + n2], w) : cmul(v[Q * k1 + n2], w);
+            v[Q * k1 + n2] = cmul_q(v[Q * k1 + n2], wq<R, INV>((n2 * k1) % R));
         }
     // Q-point DFTs over n2: X(k1 + P k2) -> v[Q k1 + k2]
 #pragma unroll
@@ -114,9 +130,42 @@ __host__ __device__ constexpr int ct_pad(int i) { return S ? i + (i >> S) : i; }
 // lines per load; a [k][r] layout still strides lanes by R float2.)
 __host__ __device__ constexpr int tw_rs(int R) { return R - 1; }
 
+// Twiddle multiply by a table entry. float2 tables hold w = (c, s) and the
+// inverse uses conj(w); float4 tables hold (c, s, -s, c) of the entry already
+// conjugated for an inverse table, so the product is one FMUL2 + one FFMA2
+// with no operand swaps or negations: a w = a.x (c, s) + a.y (-s, c).
+template <bool INV>
+__device__ __forceinline__ float2 tw_mul(float2 a, const float2* p) {
+    const float2 w = __ldg(p);
+    return INV ? cmulc(a, w) : cmul(a, w);
+}
+template <bool INV>
+__device__ __forceinline__ float2 tw_mul(float2 a, const float4* p) {
+    return cmul_q(a, __ldg(p));
+}
+
+// Computed twiddles (no table): w = exp(-+2 pi i k / L) from one fast
+// __sincosf (|angle| < 2 pi / R, abs error ~4e-7) and its powers w^2..w^(R-1)
+// by complex products of depth <= 3. Used where the shared-memory carve-out
+// leaves too little L1 for the tables (the streamed rho pass); the twiddle
+// error (< 4e-6) is far below the 1e-4 parity bar.
+struct TwSincos {};
+
+template <int R, bool INV>
+__device__ __forceinline__ void tw_apply_sincos(float2* v, int k, int L) {
+    float sn, cs;
+    __sincosf((INV ? 6.283185307179586f : -6.283185307179586f) * (float(k) / float(L)), &sn, &cs);
+    float2 p[R];
+    p[1] = make_float2(cs, sn);
+#pragma unroll
+    for (int r = 2; r < R; ++r) p[r] = cmul(p[r / 2], p[r - r / 2]);
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], p[r]);
+}
+
 // One in-place pass of radix R at Stockham stride NS over a padded buffer.
-template <int N, int T, int S, int R, int NS, int OFF, bool INV>
-__device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ twp, int tid) {
+template <int N, int T, int S, int R, int NS, int OFF, bool INV, class TW>
+__device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, int tid) {
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
     float2 v[NB][R];
@@ -134,13 +183,12 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
         const int b = tid + i * T;
         if (b < B) {
             const int k = b % NS;
-            if (NS > 1) {
-                const float2* tw = pinned(twp + (OFF + k));  // one base; the r offsets fold into the loads
+            if constexpr (NS > 1 && std::is_same<TW, TwSincos>::value) {
+                tw_apply_sincos<R, INV>(v[i], k, NS * R);
+            } else if constexpr (NS > 1) {
+                const TW* tw = pinned(twp + (OFF + k));  // one base; the r offsets fold into the loads
 #pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    const float2 w = __ldg(tw + (r - 1) * NS);
-                    v[i][r] = INV ? cmulc(v[i][r], w) : cmul(v[i][r], w);
-                }
+                for (int r = 1; r < R; ++r) v[i][r] = tw_mul<INV>(v[i][r], tw + (r - 1) * NS);
             }
             Dft<R, INV>::run(v[i]);
             const int base = (b - k) * R + k;
@@ -151,8 +199,8 @@ __device__ __forceinline__ void ct_pass(float2* x, const float2* __restrict__ tw
     __syncthreads();
 }
 
-template <int N, int T, int S, bool INV, int NS, int OFF, int R, int... Rest>
-__device__ __forceinline__ void ct_run(float2* x, const float2* twp, int tid) {
+template <int N, int T, int S, bool INV, int NS, int OFF, int R, int... Rest, class TW>
+__device__ __forceinline__ void ct_run(float2* x, const TW* twp, int tid) {
     ct_pass<N, T, S, R, NS, OFF, INV>(x, twp, tid);
     if constexpr (sizeof...(Rest) > 0)
         ct_run<N, T, S, INV, NS * R, OFF + (NS > 1 ? NS * tw_rs(R) : 0), Rest...>(x, twp, tid);
@@ -174,11 +222,36 @@ void ct_twiddles(std::vector<float2>& out) {
     if constexpr (sizeof...(Rest) > 0) ct_twiddles<N, NS * R, Rest...>(out);
 }
 
+// float4 form of a float2 table for tw_mul: (c, s, -s, c) of w, or of conj(w)
+// for a table read by inverse passes.
+inline std::vector<float4> tw4(const std::vector<float2>& t, bool conj) {
+    std::vector<float4> o(t.size());
+    for (size_t i = 0; i < t.size(); ++i) {
+        const float c = t[i].x, s = conj ? -t[i].y : t[i].y;
+        o[i] = make_float4(c, s, -s, c);
+    }
+    return o;
+}
+
+// Twiddle source of the compile-time plans: the per-pass table, or computed
+// (LPR_CT_TW_SINCOS) so the tables do not compete with the gather for L1.
+#ifndef LPR_CT_TW_SINCOS
+#define LPR_CT_TW_SINCOS 1
+#endif
+__device__ __forceinline__ auto ct_tw(const FftDesc& d) {
+#if LPR_CT_TW_SINCOS
+    (void)d;
+    return static_cast<const TwSincos*>(nullptr);
+#else
+    return d.twp;
+#endif
+}
+
 template <int R1, int... Rest>
 struct RadixPack {
     static constexpr int first = R1;
-    template <int N, int T, int S, bool INV>
-    __device__ __forceinline__ static void tail(float2* x, const float2* twp, int tid) {
+    template <int N, int T, int S, bool INV, class TW>
+    __device__ __forceinline__ static void tail(float2* x, const TW* twp, int tid) {
         if constexpr (sizeof...(Rest) > 0) ct_run<N, T, S, INV, R1, 0, Rest...>(x, twp, tid);
     }
 };
@@ -202,7 +275,7 @@ struct CtFft {
     __host__ __device__ static int elems(const FftDesc&) { return kElems; }
     template <bool INV>
     __device__ __forceinline__ static float2* run(float2* x, float2*, const FftDesc& d, int gtid) {
-        ct_run<N, T, S, INV, 1, 0, R...>(x, d.twp, gtid);
+        ct_run<N, T, S, INV, 1, 0, R...>(x, ct_tw(d), gtid);
         return x;
     }
     // first radix, and the remaining passes for kernels that run the first
@@ -210,7 +283,7 @@ struct CtFft {
     static constexpr int kR1 = RadixPack<R...>::first;
     template <bool INV>
     __device__ __forceinline__ static void run_tail(float2* x, const FftDesc& d, int gtid) {
-        RadixPack<R...>::template tail<N, T, S, INV>(x, d.twp, gtid);
+        RadixPack<R...>::template tail<N, T, S, INV>(x, ct_tw(d), gtid);
     }
     static std::vector<float2> pass_twiddles() {
         std::vector<float2> t;
@@ -227,8 +300,8 @@ struct CtFft {
 // spectral multiply between them (one shared round trip instead of three).
 
 // Forward last pass (radix R at NS = N / R) x multiplier x inverse first pass.
-template <int N, int T, int S, int R, int OFF>
-__device__ __forceinline__ void ct_mid_fused(float2* x, const float2* __restrict__ twp, const float2* ms, int tid) {
+template <int N, int T, int S, int R, int OFF, class TW>
+__device__ __forceinline__ void ct_mid_fused(float2* x, const TW* __restrict__ twp, const float2* ms, int tid) {
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
     float2 v[NB][R];
@@ -245,9 +318,13 @@ __device__ __forceinline__ void ct_mid_fused(float2* x, const float2* __restrict
     for (int i = 0; i < NB; ++i) {
         const int b = tid + i * T;
         if (b < B) {
-            const float2* tw = pinned(twp + (OFF + b));
+            if constexpr (std::is_same<TW, TwSincos>::value) {
+                tw_apply_sincos<R, false>(v[i], b, N);
+            } else {
+                const TW* tw = pinned(twp + (OFF + b));
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], __ldg(tw + (r - 1) * B));
+                for (int r = 1; r < R; ++r) v[i][r] = tw_mul<false>(v[i][r], tw + (r - 1) * B);
+            }
             Dft<R, false>::run(v[i]);
             float2 u[R];
 #pragma unroll
@@ -272,8 +349,8 @@ __device__ __forceinline__ void ct_mid_fused(float2* x, const float2* __restrict
 // Inverse last pass (radix R at NS = N / R) straight from registers to a
 // global row: butterfly b writes out[b + r NS], coalesced across the warp.
 // The buffer is free for the next TMA load once this returns.
-template <int N, int T, int S, int R, int OFF>
-__device__ __forceinline__ void ct_last_to_global(const float2* x, const float2* __restrict__ twp,
+template <int N, int T, int S, int R, int OFF, class TW>
+__device__ __forceinline__ void ct_last_to_global(const float2* x, const TW* __restrict__ twp,
                                                   float2* __restrict__ out, int tid) {
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
@@ -291,9 +368,13 @@ __device__ __forceinline__ void ct_last_to_global(const float2* x, const float2*
     for (int i = 0; i < NB; ++i) {
         const int b = tid + i * T;
         if (b < B) {
-            const float2* tw = pinned(twp + (OFF + b));
+            if constexpr (std::is_same<TW, TwSincos>::value) {
+                tw_apply_sincos<R, true>(v[i], b, N);
+            } else {
+                const TW* tw = pinned(twp + (OFF + b));
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[i][r] = cmulc(v[i][r], __ldg(tw + (r - 1) * B));
+                for (int r = 1; r < R; ++r) v[i][r] = tw_mul<true>(v[i][r], tw + (r - 1) * B);
+            }
             Dft<R, true>::run(v[i]);
 #pragma unroll
             for (int r = 0; r < R; ++r) out[b + r * B] = v[i][Dft<R, true>::slot(r)];
@@ -309,7 +390,7 @@ struct RhoStream {
     static constexpr int kElems = (ct_pad<S>(N - 1) + 2) / 2 * 2;  // even: every buffer starts 16-byte aligned
     // forward (R1, R2, R3 + fused) then inverse (R2, R1 to global); the whole
     // per-row convolution on a buffer whose row has landed
-    __device__ __forceinline__ static void convolve(float2* x, const float2* twf, const float2* twi, const float2* ms,
+    __device__ __forceinline__ static void convolve(float2* x, const float4* twf, const float4* twi, const float2* ms,
                                                     float2* out, int tid) {
         ct_pass<N, T, S, R1, 1, 0, false>(x, twf, tid);
         ct_pass<N, T, S, R2, R1, 0, false>(x, twf, tid);
@@ -317,15 +398,49 @@ struct RhoStream {
         ct_pass<N, T, S, R2, R3, 0, true>(x, twi, tid);
         ct_last_to_global<N, T, S, R1, R3 * (R2 - 1)>(x, twi, out, tid);
     }
-    static std::vector<float2> fwd_twiddles() {
+    static std::vector<float4> fwd_twiddles() {
         std::vector<float2> t;
         ct_twiddles<N, 1, R1, R2, R3>(t);
-        return t;
+        return tw4(t, false);
     }
-    static std::vector<float2> inv_twiddles() {
+    static std::vector<float4> inv_twiddles() {
         std::vector<float2> t;
         ct_twiddles<N, 1, R3, R2, R1>(t);
-        return t;
+        return tw4(t, true);
+    }
+};
+
+// Same with four radices: forward R1..R3 + fused R4, inverse R3, R2 + R1 to global.
+// Smaller radices give more butterflies per pass, so more threads (warps) per row.
+template <int N, int T, int S, int R1, int R2, int R3, int R4>
+struct RhoStream4 {
+    static constexpr int kN = N;
+    static constexpr int kT = T;
+    static constexpr int kElems = (ct_pad<S>(N - 1) + 2) / 2 * 2;
+    __device__ __forceinline__ static void convolve(float2* x, const float4* twf4, const float4* twi4, const float2* ms,
+                                                    float2* out, int tid) {
+#if LPR_RHO_TW_TABLE
+        const float4 *twf = twf4, *twi = twi4;
+#else
+        const TwSincos *twf = nullptr, *twi = nullptr;
+#endif
+        ct_pass<N, T, S, R1, 1, 0, false>(x, twf, tid);
+        ct_pass<N, T, S, R2, R1, 0, false>(x, twf, tid);
+        ct_pass<N, T, S, R3, R1 * R2, R1 * (R2 - 1), false>(x, twf, tid);
+        ct_mid_fused<N, T, S, R4, R1 * (R2 - 1) + R1 * R2 * (R3 - 1)>(x, twf, ms, tid);
+        ct_pass<N, T, S, R3, R4, 0, true>(x, twi, tid);
+        ct_pass<N, T, S, R2, R4 * R3, R4 * (R3 - 1), true>(x, twi, tid);
+        ct_last_to_global<N, T, S, R1, R4 * (R3 - 1) + R4 * R3 * (R2 - 1)>(x, twi, out, tid);
+    }
+    static std::vector<float4> fwd_twiddles() {
+        std::vector<float2> t;
+        ct_twiddles<N, 1, R1, R2, R3, R4>(t);
+        return tw4(t, false);
+    }
+    static std::vector<float4> inv_twiddles() {
+        std::vector<float2> t;
+        ct_twiddles<N, 1, R4, R3, R2, R1>(t);
+        return tw4(t, true);
     }
 };
 
@@ -358,6 +473,10 @@ using Fft4374 = CtFft<4374, 192, 1, 2, 0, 27, 27, 6>;
 using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, (LPR_FFT8192_P == 1 ? 2 : 1), 4, 16, 16, 16, 2>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 // streamed rho pass for N_rho = 4374 (2 rows in flight per block, 2 blocks per SM)
+#ifndef LPR_RHO_RADIX27
+using Rho4374 = RhoStream4<4374, 512, 0, 9, 9, 9, 6>;
+#else
 using Rho4374 = RhoStream<4374, 192, 0, 27, 27, 6>;
+#endif
 
 }  // namespace lpr

@@ -581,8 +581,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // purpose: in a persistent row loop ptxas keeps every pass's loop-invariant
 // state live and spills.)
 template <class F>
-__global__ void __launch_bounds__(F::kT, 2) k_rho_stream(const __grid_constant__ DevGeom g, const float2* __restrict__ twf,
-                                                         const float2* __restrict__ twi, const float2* __restrict__ mult,
+__global__ void __launch_bounds__(F::kT, 2) k_rho_stream(const __grid_constant__ DevGeom g, const float4* __restrict__ twf,
+                                                         const float4* __restrict__ twi, const float2* __restrict__ mult,
                                                          float2* __restrict__ spec, int items) {
     extern __shared__ __align__(16) float2 sm[];
     __shared__ __align__(8) uint64_t bars[2];
@@ -1035,16 +1035,20 @@ size_t rho_stream_smem(int variant) {
     return variant == kFft4374 ? size_t(3) * Rho4374::kElems * sizeof(float2) : 0;
 }
 
-std::vector<float2> rho_stream_inv_twiddles(int variant) {
-    return variant == kFft4374 ? Rho4374::inv_twiddles() : std::vector<float2>{};
+std::vector<float4> rho_stream_inv_twiddles(int variant) {
+    return variant == kFft4374 ? Rho4374::inv_twiddles() : std::vector<float4>{};
+}
+
+std::vector<float4> rho_stream_fwd_twiddles(int variant) {
+    return variant == kFft4374 ? Rho4374::fwd_twiddles() : std::vector<float4>{};
 }
 
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec) {
-    if (L.rho_stream && fd.twp_inv != nullptr) {
+    if (L.rho_stream && fd.twp_inv != nullptr && fd.twp_sfwd != nullptr) {
         const int items = int(grid.y);
         if (L.variant == kFft4374) {
-            k_rho_stream<Rho4374><<<int(grid.x) * ((items + 1) / 2), Rho4374::kT, rho_stream_smem(kFft4374), st>>>(g, fd.twp, fd.twp_inv,
+            k_rho_stream<Rho4374><<<int(grid.x) * ((items + 1) / 2), Rho4374::kT, rho_stream_smem(kFft4374), st>>>(g, fd.twp_sfwd, fd.twp_inv,
                                                                                                 mult, spec, items);
             return;
         }

@@ -17,7 +17,7 @@ constexpr int kMaxSectors = 16;
 // 32 bytes: two spline tap rows per LDG.256, so a sample is 2 loads),
 // 4 = quad taps (one 16-byte load per tap row), 1 = plain fp32 raster.
 #ifndef LPR_TAPS
-#define LPR_TAPS 8
+#define LPR_TAPS 4
 #endif
 struct __align__(32) Octo {
     float4 lo, hi;
@@ -75,7 +75,8 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
                             const Tap* qf, float2* spec, int tex);  // tex: 0 soft taps, 1 hw bilinear, 2 tld4 exact taps
 void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out);
 size_t rho_stream_smem(int variant);  // 0: no streamed rho kernel for this length
-std::vector<float2> rho_stream_inv_twiddles(int variant);
+std::vector<float4> rho_stream_inv_twiddles(int variant);
+std::vector<float4> rho_stream_fwd_twiddles(int variant);
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec);
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
