@@ -66,6 +66,31 @@ constexpr int kIW = 16;                   // warm-up samples per side
 constexpr int kIR = kIT + 2 * kIW;        // staged rows
 constexpr int kIC = kIT + 3 + 2 * kIW;    // staged columns (quad needs 3 more)
 constexpr int kICP = kIC + 2;             // odd row pitch (101): row- and column-walks are conflict-free
+constexpr int kIQ = (kIC + 3) / 4;        // 16-byte words per staged row on the interior fast path (25)
+
+// Stage R rows of Q float4 (row stride `ld` floats, 16-byte aligned source) into
+// shared rows of pitch P floats: every load of the thread issued before any store.
+template <int R, int Q, int P, int T>
+__device__ __forceinline__ void stage_rows(float* s, const float* __restrict__ src, int ld, int tid) {
+    constexpr int TOT = R * Q, PER = (TOT + T - 1) / T;
+    float4 v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int idx = tid + u * T;
+        if (idx < TOT) v[u] = __ldg(reinterpret_cast<const float4*>(src + size_t(idx / Q) * ld) + idx % Q);
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int idx = tid + u * T;
+        if (idx < TOT) {
+            float* d = s + (idx / Q) * P + 4 * (idx % Q);
+            d[0] = v[u].x;
+            d[1] = v[u].y;
+            d[2] = v[u].z;
+            d[3] = v[u].w;
+        }
+    }
+}
 
 template <class T>
 __global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float* __restrict__ img, T* __restrict__ q4) {
@@ -77,9 +102,15 @@ __global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float
     const int x0 = blockIdx.x * kIT, y0 = blockIdx.y * kIT, b = blockIdx.z;
     const float* src = img + size_t(b) * N * N;
     const int vx0 = x0 - kApron - kIW, vy0 = y0 - kApron - kIW;
-    for (int idx = tid; idx < kIR * kIC; idx += blockDim.x) {
-        const int i = idx / kIC, j = idx % kIC;
-        s[i][j] = __ldg(src + size_t(mirror_idx(vy0 + i, N)) * N + mirror_idx(vx0 + j, N));
+    if (vx0 >= 0 && vx0 + 4 * kIQ <= N && vy0 >= 0 && vy0 + kIR <= N && (N & 3) == 0 &&
+        (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        // interior tile (no mirroring): all of a thread's 16-byte loads in flight at once
+        stage_rows<kIR, kIQ, kICP, 128>(&s[0][0], src + size_t(vy0) * N + vx0, N, tid);
+    } else {
+        for (int idx = tid; idx < kIR * kIC; idx += blockDim.x) {
+            const int i = idx / kIC, j = idx % kIC;
+            s[i][j] = __ldg(src + size_t(mirror_idx(vy0 + i, N)) * N + mirror_idx(vx0 + j, N));
+        }
     }
     __syncthreads();
     if (tid < kIR) {  // rows
@@ -141,9 +172,14 @@ __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const flo
     const int N = g.N;
     const int c0col = blockIdx.x * kSCols, i0 = blockIdx.y * kSRows, b = blockIdx.z;
     const int rows = min(kSRows, g.n_theta - i0);
-    for (int idx = tid; idx < rows * L; idx += blockDim.x) {
-        const int i = idx / L, j = idx % L;
-        s[i][j] = __ldg(sino + (size_t(b) * g.n_theta + i0 + i) * N + mirror_idx(c0col - kIW + j, N));
+    if (rows == kSRows && c0col - kIW >= 0 && c0col - kIW + L <= N && (N & 3) == 0 &&
+        (reinterpret_cast<uintptr_t>(sino) & 15) == 0) {
+        stage_rows<kSRows, L / 4, kSP, 128>(&s[0][0], sino + (size_t(b) * g.n_theta + i0) * N + c0col - kIW, N, tid);
+    } else {
+        for (int idx = tid; idx < rows * L; idx += blockDim.x) {
+            const int i = idx / L, j = idx % L;
+            s[i][j] = __ldg(sino + (size_t(b) * g.n_theta + i0 + i) * N + mirror_idx(c0col - kIW + j, N));
+        }
     }
     __syncthreads();
     if (tid < rows) {
