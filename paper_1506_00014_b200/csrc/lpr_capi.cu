@@ -249,6 +249,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     g.Lf = 2 * g.nf;
     g.L2 = 2 * G.nts;
     g.win = G.nts + 8;
+    g.lps = (G.n_rho + 3) / 4 * 4;
     g.j0 = -G.nts / 2 - 4;
     g.pitch = G.N + 2 * kApron;
     g.aR = float(G.a_R);
@@ -393,7 +394,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     p->qg = p->dalloc<float>(B * G.n_theta * G.N);
     p->fsino = p->dalloc<float>(B * G.n_theta * G.N);
     p->spec = p->dalloc<float2>(B * G.M * (nts + 1) * nr);
-    p->lp = p->dalloc<float>(B * G.M * g.win * nr);
+    p->lp = p->dalloc<float>(B * G.M * g.win * size_t(g.lps));
     const size_t io = B * std::max<size_t>(size_t(G.N) * G.N, size_t(G.n_theta) * G.N);
     p->d_in = p->dalloc<float>(io);
     p->d_out = p->dalloc<float>(io);
@@ -434,7 +435,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         ck(cudaCreateTextureObject(&p->qtex, &rd, &td, nullptr), "cudaCreateTextureObject");
         p->g.qtex = p->qtex;
     }
-    set_smem((const void*)k_radon_out, size_t(nr) * sizeof(float));
+    set_smem((const void*)k_radon_out, size_t(g.lps) * sizeof(float));
     set_smem((const void*)k_radon_out_T, size_t(nr) * sizeof(float));
 
 }
@@ -456,7 +457,7 @@ void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStr
     mark(p, 3, st);
     launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->spec, p->lp);
     mark(p, 4, st);
-    k_radon_out<<<dim3(g.n_theta, nb), 256, g.n_rho * sizeof(float), st>>>(g, p->lp, sino);
+    k_radon_out<<<dim3(g.n_theta, nb), 256, g.lps * sizeof(float), st>>>(g, p->lp, sino);
     mark(p, 5, st);
     check_launch("radon launch");
     p->launches += 5;

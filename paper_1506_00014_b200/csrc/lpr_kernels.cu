@@ -672,13 +672,13 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
     __syncthreads();
     float2* res = F::template run<true>(sms(G.g), fft_scratch<F>(sms(G.g), fd), fd, G.tid);
     const Slots rs = result_slots<F>(smem, E, res);
-    float* out = lp + item * size_t(g.win) * n;
+    float* out = lp + item * size_t(g.win) * g.lps;
     for (int e = threadIdx.x; e < g.win * P; e += blockDim.x) {
         const int r = e / P, p = e % P;
         const int l = l0b + 2 * p;
         if (l >= n) continue;
         const float2 z = rs(p)[F::idx(wrapi(g.j0 + r, L2))];
-        float* dst = out + size_t(r) * n + l;
+        float* dst = out + size_t(r) * g.lps + l;
         if (l + 1 < n && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
             *reinterpret_cast<float2*>(dst) = z;
         } else {
@@ -701,8 +701,9 @@ __global__ void k_radon_out(DevGeom g, const float* __restrict__ lp, float* __re
     const int m = k % g.M;
     const bool flip = ((k - m) / g.M) & 1;
     const int j = i - k * nts;
-    const float* src = lp + ((size_t(b) * g.M + m) * g.win + (j - g.j0)) * n;
-    for (int l = threadIdx.x; l < n; l += blockDim.x) srow[l] = src[l];
+    const float* src = lp + ((size_t(b) * g.M + m) * g.win + (j - g.j0)) * g.lps;
+    for (int l = threadIdx.x; l < g.lps / 4; l += blockDim.x)  // rows are 16-byte aligned (lps % 4 == 0)
+        reinterpret_cast<float4*>(srow)[l] = __ldg(reinterpret_cast<const float4*>(src) + l);
     __syncthreads();
     const float cth = __ldg(g.coarse_cos + j + nts / 2) * g.one_m_aR;
     const float sgn = flip ? -1.f : 1.f;
@@ -822,12 +823,12 @@ __global__ void LPR_LB(F) k_theta_fwd_T(const __grid_constant__ DevGeom g, const
         float2* sm = smem + G.g * E;
         for (int i = G.tid; i < nts; i += G.size) sm[F::idx(nts / 2 + i)] = make_float2(0.f, 0.f);
     }
-    const float* in = lp + (size_t(b) * g.M + m) * size_t(g.win) * n;
+    const float* in = lp + (size_t(b) * g.M + m) * size_t(g.win) * g.lps;
     for (int e = threadIdx.x; e < nts * P; e += blockDim.x) {
         const int jj = e / P, p = e % P;
         const int l = l0b + 2 * p;
         const int j = jj - nts / 2;
-        const float* row = in + size_t(j - g.j0) * n;
+        const float* row = in + size_t(j - g.j0) * g.lps;
         const float a = l < n ? row[l] : 0.f, c = l + 1 < n ? row[l + 1] : 0.f;
         smem[p * E + F::idx(j < 0 ? j + L2 : j)] = make_float2(a, c);
     }
@@ -943,13 +944,13 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         float wt[4], wr[4];
         bsw(tt - kt, wt);
         bsw(tr - kr, wr);
-        const float* base = lp + (size_t(b) * g.M + m) * size_t(g.win) * n + (int(kt) - 1 - g.j0) * n;
+        const float* base = lp + (size_t(b) * g.M + m) * size_t(g.win) * g.lps + (int(kt) - 1 - g.j0) * g.lps;
         const int c0 = int(kr) - 1;
         float sacc = 0.f;
         if (c0 >= 0 && c0 + 3 < n) {  // no rho wrap (all but the last columns)
             const float* row = base + c0;
 #pragma unroll
-            for (int a = 0; a < 4; ++a, row += n)
+            for (int a = 0; a < 4; ++a, row += g.lps)
                 sacc = fmaf(wt[a], fmaf(wr[0], __ldg(row), fmaf(wr[1], __ldg(row + 1), fmaf(wr[2], __ldg(row + 2), wr[3] * __ldg(row + 3)))), sacc);
         } else {
             int cidx[4];
@@ -960,7 +961,7 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
             }
             const float* row = base;
 #pragma unroll
-            for (int a = 0; a < 4; ++a, row += n) {
+            for (int a = 0; a < 4; ++a, row += g.lps) {
                 const float v = fmaf(wr[0], __ldg(row + cidx[0]),
                                      fmaf(wr[1], __ldg(row + cidx[1]), fmaf(wr[2], __ldg(row + cidx[2]), wr[3] * __ldg(row + cidx[3]))));
                 sacc = fmaf(wt[a], v, sacc);

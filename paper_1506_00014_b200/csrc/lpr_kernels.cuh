@@ -41,6 +41,7 @@ struct DevGeom {
     int win;     // rows kept from the coarse theta inverse
     int j0;      // coarse theta index of window row 0 (= -nts/2 - 4)
     int pitch;   // row pitch of the apron image (N + 2 kApron)
+    int lps;     // row stride of the theta-inverse window buffer lp (n_rho rounded up to 4: 16-byte rows)
     float aR, inv_aR, one_m_aR, aR2, log_ar, inv_drho, inv_dtheta_p, out_scale;
     float cosm[kMaxSectors], sinm[kMaxSectors];
     float vcm[kMaxSectors], vrm[kMaxSectors];  // pixel coords of T_m^{-1}(0): (N/2)(1 - (cos, sin)(m beta)(1 - aR)/aR)

@@ -60,7 +60,7 @@ __global__ void k_radon_out_T(DevGeom g, const float* __restrict__ sino, float* 
         }
     }
     __syncthreads();
-    float* dst = lp + ((size_t(b) * g.M + m) * g.win + (j - g.j0)) * n;
+    float* dst = lp + ((size_t(b) * g.M + m) * g.win + (j - g.j0)) * g.lps;
     for (int l = threadIdx.x; l < n; l += blockDim.x) dst[l] = srow[l];
 }
 
