@@ -143,6 +143,14 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+# stage name (lpr_gpu_profile_stages) -> the kernel(s) that implement it
+STAGE_KERNELS = {
+    "prefilter_2d": ("k_prefilter_2d_iir",),
+    "prefilter_sino": ("k_prefilter_sino_iir",),
+    "rho_pass": ("k_rho_stream", "k_rho_pass"),
+}
+
+
 def ncu_traffic(stage: str, slices: int):
     """dram__bytes_read + dram__bytes_write of `stage`'s kernel from the latest
     committed `ncu --set full` capture (profiles/*/ncu_dram_bytes.json, per
@@ -156,8 +164,9 @@ def ncu_traffic(stage: str, slices: int):
                 per = json.load(f)["per_slice_bytes"]
         except Exception:
             continue
+        kernels = STAGE_KERNELS.get(stage, ("k_" + stage,))
         for name, b in per.items():
-            if name == "k_" + stage or name.startswith("k_" + stage + "<"):
+            if any(name == k or name.startswith(k + "<") for k in kernels):
                 return b * slices
     return None
 

@@ -550,7 +550,8 @@ void run_host(lpr_gpu_plan* p, ChunkFn fn, const float* hin, float* hout, int ba
     const bool pin_in = is_pinned(hin), pin_out = is_pinned(hout);
     cudaStream_t st = p->stream;
     if (pin_in && pin_out && batch > 1 && p->max_batch > 1) {
-        const int c = std::max(1, std::min(p->max_batch / 2, (batch + 3) / 4));
+        // ~8 chunks: the exposed pipeline fill (first H2D) and drain (last D2H) shrink with the chunk
+        const int c = std::max(1, std::min(p->max_batch / 2, (batch + 7) / 8));
         const int chunks = (batch + c - 1) / c;
         for (int i = 0; i < chunks; ++i) {
             const int slot = i & 1, b0 = i * c, nb = std::min(c, batch - b0);

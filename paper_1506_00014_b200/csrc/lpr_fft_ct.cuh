@@ -470,7 +470,10 @@ using Fft4374 = CtFft<4374, 192, 1, 2, 0, 27, 27, 6>;
 #ifndef LPR_FFT8192_P
 #define LPR_FFT8192_P 1  // column pairs per block of the fine theta kernels (A/B knob)
 #endif
-using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, (LPR_FFT8192_P == 1 ? 2 : 1), 4, 16, 16, 16, 2>;
+#ifndef LPR_FFT8192_MINB
+#define LPR_FFT8192_MINB (LPR_FFT8192_P == 1 ? 2 : 1)
+#endif
+using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16, 2>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 // streamed rho pass for N_rho = 4374 (2 rows in flight per block, 2 blocks per SM)
 #ifndef LPR_RHO_RADIX27
