@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-LPR_GPU_LIB=$PWD/paper_1506_00014_b200/liblpradon_gpu_mb3.so python scripts/stage_times.py 2048 16 > gpurun_out/st_mb3.json
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest.txt
+python scripts/stage_times.py 2048 16 > gpurun_out/st_new.json

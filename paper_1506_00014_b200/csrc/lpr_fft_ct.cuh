@@ -268,6 +268,9 @@ struct CtFft {
     static constexpr int kT = T;
     static constexpr int kP = P;
     static constexpr int kMinBlocks = MINB;
+    // radices covering only N/2: the final radix-2 pass is left to the caller
+    // (the fine theta kernel fuses it into its band-limited store)
+    static constexpr bool kLast2 = (R * ...) * 2 == N;
     // per-transform slots, rounded to 4 mod 16 so the kP buffers of a block
     // start on different banks (row loads spread consecutive lanes over them)
     static constexpr int kElems = (ct_pad<S>(N - 1) + 1 + 12) / 16 * 16 + 4;
@@ -474,6 +477,8 @@ using Fft4374 = CtFft<4374, 192, 1, 2, 0, 27, 27, 6>;
 #define LPR_FFT8192_MINB (LPR_FFT8192_P == 1 ? 2 : 1)
 #endif
 using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16, 2>;
+// the fine theta forward of R: same plan without the last radix-2 pass
+using Fft8192Band = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 // streamed rho pass for N_rho = 4374 (2 rows in flight per block, 2 blocks per SM)
 #ifndef LPR_RHO_RADIX27

@@ -274,6 +274,40 @@ __device__ __forceinline__ void store_half_spectra(Slots res, int L, int nts, in
     }
 }
 
+// Same, for a plan whose final radix-2 pass (NS = L/2) was not run: only the
+// outputs |k| < nts are needed, so each is finished here from the four
+// inputs of its two radix-2 butterflies: Z(k) = x[k] + w x[k + L/2] and
+// Z(L - k) = x[L/2 - k] + conj(w) x[L - k], w = exp(-2 pi i k / L).
+template <class F>
+__device__ __forceinline__ void store_half_spectra_r2(Slots res, int L, int nts, int n_rho, int l0b,
+                                                      float2* __restrict__ out) {
+    constexpr int P = F::kP;
+    const int H = L / 2;
+    for (int e = threadIdx.x; e < (nts + 1) * P; e += blockDim.x) {
+        const int k = e / P, p = e % P;
+        const int l = l0b + 2 * p;
+        if (l >= n_rho) continue;
+        float2 A = make_float2(0.f, 0.f), B = A;
+        if (k < nts) {
+            float sn, cs;
+            __sincosf(-6.283185307179586f * (float(k) / float(L)), &sn, &cs);
+            const float2 w = make_float2(cs, sn);
+            const float2* x = res(p);
+            const float2 z = cadd(x[F::idx(k)], cmul(x[F::idx(k + H)], w));
+            const float2 zm = k == 0 ? z : cadd(x[F::idx(H - k)], cmulc(x[F::idx(L - k)], w));
+            A = make_float2(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y));
+            B = make_float2(0.5f * (z.y + zm.y), -0.5f * (z.x - zm.x));
+        }
+        float2* dst = out + size_t(k) * n_rho + l;
+        if (l + 1 < n_rho && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            *reinterpret_cast<float4*>(dst) = make_float4(A.x, A.y, B.x, B.y);
+        } else {
+            dst[0] = A;
+            if (l + 1 < n_rho) dst[1] = B;
+        }
+    }
+}
+
 // Load half spectra rows k in [0, kmax) of the block's pairs and rebuild each
 // packed Hermitian transform of length L: Z(k) = A + iB, Z(L-k) = conj(A) + i conj(B).
 template <class F>
@@ -510,7 +544,10 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
             F::template run_tail<false>(sm, fd, G.tid);
 #endif
             float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
-            store_half_spectra<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out);
+            if constexpr (F::kLast2)
+                store_half_spectra_r2<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out);
+            else
+                store_half_spectra<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out);
             return;
         }
     }
@@ -1028,6 +1065,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
         cudaError_t r = smem_attr((const void*)K, L);                          \
         if (r != cudaSuccess) e = r;                                           \
     } while (0)
+    if (fine.variant == kFft8192) SET(k_radon_theta_fwd<Fft8192Band>, fine.smem * fine.per_block);
 #define FINE(F)                                                   \
     SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block);         \
     SET((k_radon_theta_fwd<F, 1>), fine.smem * fine.per_block);    \
@@ -1064,6 +1102,10 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
         return;
     }
 #define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
+    if (L.variant == kFft8192) {
+        CALL(Fft8192Band);
+        return;
+    }
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }
