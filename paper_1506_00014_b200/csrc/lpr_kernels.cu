@@ -192,9 +192,11 @@ __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const flo
         for (int k = L - 2; k >= 0; --k) r[k] = d = z * (d - r[k]);
     }
     __syncthreads();
-    for (int idx = tid; idx < rows * kSCols; idx += blockDim.x) {
-        const int i = idx / kSCols, j = idx % kSCols;
-        if (c0col + j < N) qg[(size_t(b) * g.n_theta + i0 + i) * N + c0col + j] = s[i][kIW + j];
+    // transposed store (Qg^T[b][s][theta], see gather_sino): a warp writes 32
+    // consecutive theta of one s column; the odd pitch keeps the reads conflict-free
+    for (int idx = tid; idx < kSRows * kSCols; idx += blockDim.x) {
+        const int i = idx % kSRows, j = idx / kSRows;
+        if (i < rows && c0col + j < N) qg[(size_t(b) * N + c0col + j) * g.n_theta + i0 + i] = s[i][kIW + j];
     }
 }
 
@@ -765,7 +767,10 @@ __global__ void k_radon_out(DevGeom g, const float* __restrict__ lp, float* __re
 }
 
 // ------------------------------------------------------------- R#
-__device__ __forceinline__ float gather_sino(const float* __restrict__ row, int N, float t) {
+// Qg is stored s-major (Qg^T[b][s][theta], written by k_prefilter_sino_iir):
+// the 32 lanes of a warp take 32 consecutive lattice rows at nearly the same
+// s, so each tap load is one or two cache lines instead of 32.
+__device__ __forceinline__ float gather_sino(const float* __restrict__ row, int N, float t, int ld) {
     const float kf = floorf(t);
     float w[4];
     bsw(t - kf, w);
@@ -774,7 +779,7 @@ __device__ __forceinline__ float gather_sino(const float* __restrict__ row, int 
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int idx = k0 + a;
-        if (idx >= 0 && idx < N) acc = fmaf(w[a], __ldg(row + idx), acc);
+        if (idx >= 0 && idx < N) acc = fmaf(w[a], __ldg(row + size_t(idx) * ld), acc);
     }
     return acc;
 }
@@ -803,11 +808,11 @@ __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, cons
                 int i = m * nts + j;
                 const bool flip = i < 0;
                 if (flip) i += g.n_theta;
-                const float* row = qg + (size_t(b) * g.n_theta + i) * N;
+                const float* row = qg + size_t(b) * N * g.n_theta + i;
                 const float cth = __ldg(g.coarse_cos + jj) * g.one_m_aR;
                 const float sg = flip ? -halfN : halfN;
-                return make_float2(one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN)) : 0.f,
-                                   two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN)) : 0.f);
+                return make_float2(one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f,
+                                   two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f);
             });
             F::template run_tail<false>(sm, fd, G.tid);
             float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * g.n_rho;
@@ -827,12 +832,12 @@ __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, cons
             int i = m * nts + j;
             const bool flip = i < 0;
             if (flip) i += g.n_theta;
-            const float* row = qg + (size_t(b) * g.n_theta + i) * N;
+            const float* row = qg + size_t(b) * N * g.n_theta + i;
             const float cth = __ldg(g.coarse_cos + jj) * g.one_m_aR;
             const float sg = flip ? -halfN : halfN;
             // t = (s_raster + 1/2) N with s_raster = (e^rho - (1-aR) cos) / (2 aR)
-            v[h][0] = one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN)) : 0.f;
-            v[h][1] = two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN)) : 0.f;
+            v[h][0] = one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f;
+            v[h][1] = two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f;
             slot[h] = j < 0 ? j + L2 : j;
         }
 #pragma unroll
