@@ -724,6 +724,10 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
             dst[0] = z.x;
             if (l + 1 < n) dst[1] = z.y;
         }
+        if (l < 3) {  // periodic copy of columns 0..2 past the end: rho taps never wrap
+            dst[n] = z.x;
+            if (l + 1 < 3) dst[n + 1] = z.y;
+        }
     }
 }
 
@@ -989,7 +993,19 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         const float* base = lp + (size_t(b) * g.M + m) * size_t(g.win) * g.lps + (int(kt) - 1 - g.j0) * g.lps;
         const int c0 = int(kr) - 1;
         float sacc = 0.f;
-        if (c0 >= 0 && c0 + 3 < n) {  // no rho wrap (all but the last columns)
+        if (g.lptex) {  // four tld4 gathers (2 x 2 texels each, exact fp32)
+            const float x0 = float(c0 + 1), x1 = x0 + 2.f;
+            const float y0 = float((b * g.M + m) * g.win + int(kt) - 1 - g.j0) + 1.f, y1 = y0 + 2.f;
+            const float4 a = tex2Dgather<float4>(g.lptex, x0, y0, 0), e = tex2Dgather<float4>(g.lptex, x1, y0, 0);
+            const float4 d = tex2Dgather<float4>(g.lptex, x0, y1, 0), f = tex2Dgather<float4>(g.lptex, x1, y1, 0);
+            const float r0 = fmaf(wr[0], a.w, fmaf(wr[1], a.z, fmaf(wr[2], e.w, wr[3] * e.z)));
+            const float r1 = fmaf(wr[0], a.x, fmaf(wr[1], a.y, fmaf(wr[2], e.x, wr[3] * e.y)));
+            const float r2 = fmaf(wr[0], d.w, fmaf(wr[1], d.z, fmaf(wr[2], f.w, wr[3] * f.z)));
+            const float r3 = fmaf(wr[0], d.x, fmaf(wr[1], d.y, fmaf(wr[2], f.x, wr[3] * f.y)));
+            acc += fmaf(wt[0], r0, fmaf(wt[1], r1, fmaf(wt[2], r2, wt[3] * r3)));
+            continue;
+        }
+        if (c0 >= 0 && c0 + 3 < n + 3) {  // columns n..n+2 repeat 0..2 (k_theta_inv), so no wrap inside the disc
             const float* row = base + c0;
 #pragma unroll
             for (int a = 0; a < 4; ++a, row += g.lps)

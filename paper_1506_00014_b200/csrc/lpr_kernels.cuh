@@ -41,7 +41,7 @@ struct DevGeom {
     int win;     // rows kept from the coarse theta inverse
     int j0;      // coarse theta index of window row 0 (= -nts/2 - 4)
     int pitch;   // row pitch of the apron image (N + 2 kApron)
-    int lps;     // row stride of the theta-inverse window buffer lp (n_rho rounded up to 4: 16-byte rows)
+    int lps;     // row stride of the theta-inverse window buffer lp: n_rho + 3 periodic columns, rounded up to 4 (16-byte rows)
     float aR, inv_aR, one_m_aR, aR2, log_ar, inv_drho, inv_dtheta_p, out_scale;
     float cosm[kMaxSectors], sinm[kMaxSectors];
     float vcm[kMaxSectors], vrm[kMaxSectors];  // pixel coords of T_m^{-1}(0): (N/2)(1 - (cos, sin)(m beta)(1 - aR)/aR)
@@ -53,6 +53,7 @@ struct DevGeom {
     const float* erho;        // n_rho entries: exp(log a_r + l drho)
     const float* fir;         // 2 kFirHalf + 1 prefilter taps
     cudaTextureObject_t qtex; // texture-gather ablation: coefficient raster (0 unless enabled)
+    cudaTextureObject_t lptex; // tld4 view of lp for k_bp_out (0 unless enabled)
 };
 
 // FFT kernel variants: a compile-time register FFT for the hot lengths
