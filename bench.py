@@ -236,7 +236,7 @@ def run_ours(args):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     g = geometry(args)
-    z, zb = lp.zeta_spectrum(g), lp.zeta_bp_spectrum(g)
+    z, zb = lp.zeta_spectrum(g, device=local), lp.zeta_bp_spectrum(g, device=local)  # plan constants (GPU fp64)
     B = args.batch
     plan = lp.RadonPlan(g, z, zb, max_batch=B, device=local)
     start, count = stack_shard(B * ws, ws, rank)  # this rank's slices of the stack (weak scaling)

@@ -1,5 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest.txt
-LPR_BP_TEX=1 timeout 900 python -m pytest tests -q -m gpu -x -k "parity or gaussian or fbp" 2>&1 | tail -3 > gpurun_out/pytest_tex.txt
-python scripts/stage_times.py 2048 16 > gpurun_out/st_new.json
-LPR_BP_TEX=1 python scripts/stage_times.py 2048 16 > gpurun_out/st_tex.json
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_rho_stream|k_theta_inv" -c 2 -o gpurun_out/rs2 python scripts/profile_one.py > gpurun_out/rs2.log 2>&1

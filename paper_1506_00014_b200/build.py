@@ -23,10 +23,11 @@ LIB = os.path.join(PKG, "liblpradon_gpu" + (f"_{_VARIANT}" if _VARIANT else "") 
 EXTRA_DEFS = os.environ.get("LPR_DEFS", "").split() if _VARIANT else []
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_LIB = "/usr/local/cuda/lib64"  # cuFFT (plan-time fp64 spectra only, lpr_spectrum.cu)
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 
-CU_SOURCES = ["lpr_kernels.cu", "lpr_transpose.cu", "lpr_capi.cu"]
+CU_SOURCES = ["lpr_kernels.cu", "lpr_transpose.cu", "lpr_capi.cu", "lpr_spectrum.cu"]
 CXX_SOURCES = ["lpr_host.cpp"]
 
 
@@ -82,7 +83,8 @@ def build(verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=4) as ex:
         list(ex.map(lambda j: _run(*j), jobs))
     if jobs or _stale(LIB, objs):
-        _run([nvcc, "-ccbin", _host_cxx(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread"],
+        _run([nvcc, "-ccbin", _host_cxx(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread",
+              "-L" + CUDA_LIB, "-lcufft", "-Xlinker", "-rpath=" + CUDA_LIB],
              os.path.join(BUILD, "link.log"))
     if verbose:
         for src in CU_SOURCES:

@@ -18,6 +18,9 @@
 
 namespace lpr {
 
+// plan-time spectra on the GPU (lpr_spectrum.cu)
+void spectrum_gpu(int device, const lpr_geometry& g, int kind, double* out);
+
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
 __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const float* sino, float* qg);
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
@@ -295,12 +298,12 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     std::vector<double> zbuf, zbbuf;
     if (!zeta) {
         zbuf.resize(2 * rows * nr);
-        host::spectrum(G, 0, zbuf.data());
+        spectrum_gpu(p->device, G, 0, zbuf.data());
         zeta = zbuf.data();
     }
     if (!zeta_bp) {
         zbbuf.resize(2 * rows * nr);
-        host::spectrum(G, 1, zbbuf.data());
+        spectrum_gpu(p->device, G, 1, zbbuf.data());
         zeta_bp = zbbuf.data();
     }
     auto bhat = [](long k, long n) { return (2.0 + std::cos(2.0 * kPi * double(k) / double(n))) / 3.0; };
@@ -643,6 +646,14 @@ int lpr_spectrum_quadrature(const lpr_geometry* geom, int kind, double* out) {
     return guard([&] {
         if (!geom || !out || (kind != 0 && kind != 1)) throw std::invalid_argument("bad spectrum arguments");
         host::spectrum(*geom, kind, out);
+    });
+}
+
+int lpr_gpu_spectrum_quadrature(int device, const lpr_geometry* geom, int kind, double* out) {
+    return guard([&] {
+        if (!geom || !out || (kind != 0 && kind != 1)) throw std::invalid_argument("bad spectrum arguments");
+        const lpr_geometry G = host::make_geometry(geom->N, geom->M, geom->n_theta, geom->n_rho);
+        spectrum_gpu(device, G, kind, out);
     });
 }
 

@@ -40,19 +40,24 @@ def smooth_n_rho(N: int, M: int = 3) -> int:
     return v
 
 
-def _spectrum(g: Geometry, kind: int) -> np.ndarray:
+def _spectrum(g: Geometry, kind: int, device) -> np.ndarray:
     out = np.zeros((2 * g.nts, g.n_rho), dtype=np.complex128)
-    check(lib().lpr_spectrum_quadrature(ctypes.byref(g), kind, out.ctypes.data))
+    if device is None:
+        check(lib().lpr_spectrum_quadrature(ctypes.byref(g), kind, out.ctypes.data))
+    else:
+        check(lib().lpr_gpu_spectrum_quadrature(int(device), ctypes.byref(g), kind, out.ctypes.data))
     return out
 
 
-def zeta_spectrum(g: Geometry) -> np.ndarray:
-    """Forward-kernel spectrum, (2 nts) x n_rho complex, theta rows in FFT order."""
-    return _spectrum(g, 0)
+def zeta_spectrum(g: Geometry, device=None) -> np.ndarray:
+    """Forward-kernel spectrum, (2 nts) x n_rho complex, theta rows in FFT order
+    (kernel.cpp:341-439, quadrature). device=None: host fp64 threads; an int:
+    the same quadrature on that GPU (fp64)."""
+    return _spectrum(g, 0, device)
 
 
-def zeta_bp_spectrum(g: Geometry) -> np.ndarray:
-    return _spectrum(g, 1)
+def zeta_bp_spectrum(g: Geometry, device=None) -> np.ndarray:
+    return _spectrum(g, 1, device)
 
 
 class RadonPlan:
