@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_rho_stream|k_theta_inv" -c 2 -o gpurun_out/rs2 python scripts/profile_one.py > gpurun_out/rs2.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -5 > gpurun_out/pytest.txt
+python scripts/em_time.py 2048 16 10 > gpurun_out/em_time.json 2>&1

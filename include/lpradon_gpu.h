@@ -15,6 +15,8 @@
  *   lpr_gpu_radon[_host]    <- fast_radon(Image, RadonPlan) -> Sinogram
  *   lpr_gpu_backproject[_host] <- fast_backprojection(Sinogram, RadonPlan) -> Image
  *   lpr_gpu_radon_transpose <- the exact discrete adjoint used by adjoint_gap
+ *   lpr_gpu_sensitivity     <- sensitivity_image(plan)
+ *   lpr_gpu_em[_host]       <- em_run(g, plan, iters, f0) / em_step
  *
  * No C++ or CUDA types cross the boundary: plain pointers, sizes and an
  * opaque stream handle (a cudaStream_t passed as void*, NULL = default).
@@ -101,6 +103,22 @@ int lpr_gpu_radon_transpose(lpr_gpu_plan* plan, const float* d_sino, float* d_im
 int lpr_gpu_filter(lpr_gpu_plan* plan, int kind, const float* d_in, float* d_out, int batch, void* stream);
 int lpr_gpu_fbp(lpr_gpu_plan* plan, int kind, const float* d_sino, float* d_img, int batch, void* stream);
 int lpr_gpu_fbp_host(lpr_gpu_plan* plan, int kind, const float* h_sino, float* h_img, int batch);
+
+/* EM reconstruction, device resident:
+ * f <- f R#(g / max(R f, eps)) / R# chi_C with eps = 1e-6 max(g) per slice
+ * (bins under eps give ratio 0), the sensitivity floor-clamped at 1e-6 of its
+ * max, estimates kept >= 0 and 0 outside the unit disc.
+ * lpr_gpu_sensitivity: R# chi_C (one N x N image) <- sensitivity_image(plan).
+ * lpr_gpu_em: `iters` steps <- em_run(g, plan, iters, f0); d_img holds f0 on
+ * entry (init != 0: f0 = 1 inside the unit disc) and the estimate on return;
+ * h_loglik (host, batch x iters doubles, may be NULL) receives the Poisson
+ * log-likelihood sum(g log Rf - Rf) over Rf > eps of every iterate f^1..f^iters.
+ * A negative or non-finite g is LPR_ERR_ARG; a non-finite estimate LPR_ERR_CUDA. */
+int lpr_gpu_sensitivity(lpr_gpu_plan* plan, float* d_img, void* stream);
+int lpr_gpu_em(lpr_gpu_plan* plan, const float* d_sino, float* d_img, int batch, int iters, int init,
+               double* h_loglik, void* stream);
+int lpr_gpu_em_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int batch, int iters, int init,
+                    double* h_loglik);
 
 /* Same operators on host buffers: pinned staging, H2D, compute, D2H and a
  * stream synchronisation inside the call (the end-to-end path). */

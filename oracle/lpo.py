@@ -298,6 +298,43 @@ def fbp(p: Plan, zeta_bp: np.ndarray, sino: np.ndarray, kind: str = "ramp") -> n
     return C_NORM * fast_backprojection(p, zeta_bp, apply_filter(sino, kind))
 
 
+# ----------------------------------------------------------------- EM
+
+def disc_mask(N: int) -> np.ndarray:
+    """Pixels inside the unit disc: (2c - N)^2 + (2r - N)^2 <= N^2 (the R# support)."""
+    i = 2 * np.arange(N) - N
+    return (i[None, :] ** 2 + i[:, None] ** 2) <= N * N
+
+
+def sensitivity_image(p: Plan, zeta_bp: np.ndarray) -> np.ndarray:
+    """R# chi_C, chi_C = 1 on every detector bin (|s| <= 1/2)."""
+    return fast_backprojection(p, zeta_bp, np.ones((p.n_theta, p.N)))
+
+
+def em_run(p: Plan, zeta: np.ndarray, zeta_bp: np.ndarray, g: np.ndarray, iters: int, f0=None):
+    """em_run / em_step: f <- f R#(g / max(Rf, eps)) / R# chi_C,
+    eps = 1e-6 max g (bins with Rf <= eps give ratio 0), sensitivity clamped at
+    1e-6 of its max, estimate >= 0 and 0 outside the unit disc; returns the
+    estimate and the Poisson log-likelihood of every iterate f^1..f^iters."""
+    g = np.asarray(g, dtype=np.float64)
+    mask = disc_mask(p.N)
+    f = mask.astype(np.float64) if f0 is None else np.array(f0, dtype=np.float64)
+    sens = sensitivity_image(p, zeta_bp)
+    inv = np.where(mask, 1.0 / np.maximum(sens, 1e-6 * sens.max()), 0.0)
+    eps = 1e-6 * g.max()
+    hist = []
+    rf = fast_radon(p, zeta, f)
+    for _ in range(iters):
+        q = np.where(rf > eps, g / np.where(rf > eps, rf, 1.0), 0.0)
+        f = np.maximum(f * fast_backprojection(p, zeta_bp, q) * inv, 0.0)
+        if not np.isfinite(f).all():
+            raise FloatingPointError("em: non-finite estimate")
+        rf = fast_radon(p, zeta, f)
+        ok = rf > eps
+        hist.append(float(np.sum(g[ok] * np.log(rf[ok]) - rf[ok])))
+    return f, np.array(hist)
+
+
 # ----------------------------------------------------------------- inputs
 
 def smooth_disc_image(N: int, support_radius: float, seed: int, blur_sigma: float = 3.0) -> np.ndarray:

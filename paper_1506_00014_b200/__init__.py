@@ -9,6 +9,7 @@ from .lp_ops import (  # noqa: F401
     RadonPlan,
     adjoint_gap,
     apply_filter,
+    em_run,
     fast_backprojection,
     fbp,
     fast_radon,
@@ -16,6 +17,7 @@ from .lp_ops import (  # noqa: F401
     inner_sinogram,
     radon_transpose,
     sampling_plan,
+    sensitivity_image,
     smooth_n_rho,
     zeta_bp_spectrum,
     zeta_spectrum,

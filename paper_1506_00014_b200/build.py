@@ -27,7 +27,7 @@ CUDA_LIB = "/usr/local/cuda/lib64"  # cuFFT (plan-time fp64 spectra only, lpr_sp
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 
-CU_SOURCES = ["lpr_kernels.cu", "lpr_transpose.cu", "lpr_capi.cu", "lpr_spectrum.cu"]
+CU_SOURCES = ["lpr_kernels.cu", "lpr_transpose.cu", "lpr_capi.cu", "lpr_spectrum.cu", "lpr_em.cu"]
 CXX_SOURCES = ["lpr_host.cpp"]
 
 

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "lpr_host.hpp"
+#include "lpr_em.cuh"
 #include "lpr_kernels.cuh"
 #include "lpradon_gpu.h"
 
@@ -138,6 +139,10 @@ struct lpr_gpu_plan {
     cudaTextureObject_t lptex = 0;  // tld4 view of lp for the R# output resampling (LPR_BP_TEX=0: direct loads)
     std::vector<void*> allocs;
     long long launches = 0, ffts = 0;
+    // EM state (allocated on first use): Rf / ratio sinograms, R# images, the
+    // inverted sensitivity R# chi_C, per-slice max g, flags, log-likelihoods
+    float *em_rf = nullptr, *em_bp = nullptr, *em_inv_sens = nullptr, *em_gmax = nullptr;
+    int* em_bad = nullptr;
 
     template <class T>
     T* dalloc(size_t count) {
@@ -545,6 +550,46 @@ void fbp_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStrea
 
 const char* const kBackprojectStages[] = {"prefilter_sino", "bp_theta_fwd", "rho_pass", "theta_inv", "bp_out"};
 
+// ---- EM: f+ = f R#(g / max(Rf, eps)) / R#chi_C
+void em_buffers(lpr_gpu_plan* p) {
+    if (p->em_rf) return;
+    const lpr_geometry& G = p->geo;
+    p->em_rf = p->dalloc<float>(size_t(p->max_batch) * G.n_theta * G.N);
+    p->em_bp = p->dalloc<float>(size_t(p->max_batch) * G.N * G.N);
+    p->em_inv_sens = p->dalloc<float>(size_t(G.N) * G.N);
+    p->em_gmax = p->dalloc<float>(size_t(p->max_batch) + 1);
+    p->em_bad = p->dalloc<int>(1);
+    // sensitivity R# chi_C: chi_C = 1 on every bin (|s| <= 1/2 covers the detector)
+    cudaStream_t st = p->stream;
+    launch_fill(p->em_rf, size_t(G.n_theta) * G.N, 1.f, st);
+    backproject_chunk(p, p->em_rf, p->em_bp, 1, st);
+    launch_slice_max(p->em_bp, size_t(G.N) * G.N, 1, p->em_gmax, p->em_bad, st);
+    launch_sens_invert(G.N, p->em_bp, p->em_gmax, p->em_inv_sens, st);
+    check_launch("em sensitivity");
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
+// iters EM steps on nb slices: f (device, in/out), g (device); ll (device,
+// nb x iters doubles, zeroed) receives the log-likelihood of every iterate
+// f^1..f^iters (appended after each step).
+void em_chunk(lpr_gpu_plan* p, const float* g, float* f, int nb, int iters, double* ll, cudaStream_t st) {
+    const lpr_geometry& G = p->geo;
+    const size_t ps = size_t(G.n_theta) * G.N, pi = size_t(G.N) * G.N;
+    ck(cudaMemsetAsync(p->em_bad, 0, sizeof(int), st), "memset");
+    launch_slice_max(g, ps, nb, p->em_gmax, p->em_bad, st);
+    radon_chunk(p, f, p->em_rf, nb, st);
+    for (int k = 0; k < iters; ++k) {
+        // ratio for this step; its pass also scores the current iterate f^k (k >= 1)
+        launch_em_ratio(g, p->em_rf, ps, nb, p->em_gmax, k > 0 ? ll + (k - 1) : nullptr, iters, true, st);
+        backproject_chunk(p, p->em_rf, p->em_bp, nb, st);
+        launch_em_update(f, p->em_bp, p->em_inv_sens, pi, nb, p->em_bad, st);
+        radon_chunk(p, f, p->em_rf, nb, st);
+    }
+    if (iters > 0) launch_em_ratio(g, p->em_rf, ps, nb, p->em_gmax, ll + (iters - 1), iters, false, st);
+    check_launch("em launch");
+    p->launches += 2 + 3LL * iters;
+}
+
 using ChunkFn = void (*)(lpr_gpu_plan*, const float*, float*, int, cudaStream_t);
 
 void run_device(lpr_gpu_plan* p, ChunkFn fn, const float* in, float* out, int batch, size_t in_sz, size_t out_sz,
@@ -691,6 +736,91 @@ int lpr_gpu_plan_create_ex(int device, const lpr_geometry* geom, const double* z
 }
 
 void lpr_gpu_plan_destroy(lpr_gpu_plan* plan) { delete plan; }
+
+int lpr_gpu_sensitivity(lpr_gpu_plan* p, float* d_img, void* stream) {
+    return guard([&] {
+        if (!p || !d_img) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(p->device), "cudaSetDevice");
+        em_buffers(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        launch_fill(p->em_rf, size_t(p->geo.n_theta) * p->geo.N, 1.f, st);
+        backproject_chunk(p, p->em_rf, d_img, 1, st);
+        check_launch("sensitivity");
+    });
+}
+
+int lpr_gpu_em(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, int iters, int init, double* h_loglik,
+               void* stream) {
+    return guard([&] {
+        if (!p) throw std::invalid_argument("null plan");
+        if (batch < 0 || iters < 0 || (batch > 0 && (!d_sino || !d_img)))
+            throw std::invalid_argument("em: bad buffers, batch or iters");
+        ck(cudaSetDevice(p->device), "cudaSetDevice");
+        em_buffers(p);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const lpr_geometry& G = p->geo;
+        const size_t ps = size_t(G.n_theta) * G.N, pi = size_t(G.N) * G.N;
+        double* ll = nullptr;
+        ck(cudaMalloc(&ll, sizeof(double) * std::max<size_t>(1, size_t(p->max_batch) * std::max(iters, 1))), "cudaMalloc");
+        try {
+            for (int b0 = 0; b0 < batch; b0 += p->max_batch) {
+                const int nb = std::min(p->max_batch, batch - b0);
+                float* f = d_img + size_t(b0) * pi;
+                if (init) launch_disc_fill(G.N, f, nb, st);  // f0 = 1 inside the unit disc
+                ck(cudaMemsetAsync(ll, 0, sizeof(double) * size_t(nb) * std::max(iters, 1), st), "memset");
+                em_chunk(p, d_sino + size_t(b0) * ps, f, nb, iters, ll, st);
+                int bad = 0;
+                ck(cudaMemcpyAsync(&bad, p->em_bad, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+                if (h_loglik && iters > 0)
+                    ck(cudaMemcpyAsync(h_loglik + size_t(b0) * iters, ll, sizeof(double) * size_t(nb) * iters,
+                                       cudaMemcpyDeviceToHost, st),
+                       "D2H");
+                ck(cudaStreamSynchronize(st), "sync");
+                if (bad & 1) throw std::invalid_argument("em: the sinogram must be finite and nonnegative");
+                if (bad & 2) throw std::runtime_error("em: non-finite estimate");
+            }
+        } catch (...) {
+            cudaFree(ll);
+            throw;
+        }
+        cudaFree(ll);
+    });
+}
+
+int lpr_gpu_em_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batch, int iters, int init,
+                    double* h_loglik) {
+    return guard([&] {
+        if (!p) throw std::invalid_argument("null plan");
+        if (batch < 0 || (batch > 0 && (!h_sino || !h_img))) throw std::invalid_argument("em: bad buffers or batch");
+        ck(cudaSetDevice(p->device), "cudaSetDevice");
+        const lpr_geometry& G = p->geo;
+        const size_t ps = size_t(G.n_theta) * G.N, pi = size_t(G.N) * G.N;
+        float *dg = nullptr, *df = nullptr;
+        ck(cudaMalloc(&dg, sizeof(float) * ps * std::max(batch, 1)), "cudaMalloc");
+        if (cudaMalloc(&df, sizeof(float) * pi * std::max(batch, 1)) != cudaSuccess) {
+            cudaFree(dg);
+            throw Error(LPR_ERR_OOM, "cudaMalloc");
+        }
+        int rc = LPR_OK;
+        cudaStream_t st = p->stream;
+        try {
+            ck(cudaMemcpyAsync(dg, h_sino, sizeof(float) * ps * batch, cudaMemcpyHostToDevice, st), "H2D");
+            if (!init) ck(cudaMemcpyAsync(df, h_img, sizeof(float) * pi * batch, cudaMemcpyHostToDevice, st), "H2D");
+            rc = lpr_gpu_em(p, dg, df, batch, iters, init, h_loglik, st);
+            if (rc == LPR_OK) {
+                ck(cudaMemcpyAsync(h_img, df, sizeof(float) * pi * batch, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaStreamSynchronize(st), "sync");
+            }
+        } catch (...) {
+            cudaFree(dg);
+            cudaFree(df);
+            throw;
+        }
+        cudaFree(dg);
+        cudaFree(df);
+        if (rc != LPR_OK) throw Error(lpr_status(rc), g_last_error);
+    });
+}
 
 int lpr_gpu_radon(lpr_gpu_plan* p, const float* d_img, float* d_sino, int batch, void* stream) {
     return guard([&] {

@@ -205,6 +205,49 @@ def fbp(sino, plan: RadonPlan, kind: str = "ramp"):
                 lambda h, i, o, b: lib().lpr_gpu_fbp_host(h, k, i, o, b))
 
 
+def sensitivity_image(plan: RadonPlan):
+    """R# chi_C: the back-projection of the all-lines
+    indicator, N x N CUDA tensor on the plan's device."""
+    import torch
+
+    g = plan.geometry
+    out = torch.empty(g.N, g.N, dtype=torch.float32, device=f"cuda:{plan.device}")
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    check(lib().lpr_gpu_sensitivity(plan.handle, out.data_ptr(), ctypes.c_void_p(stream)))
+    return out
+
+
+def em_run(sino, plan: RadonPlan, iters: int, f0=None):
+    """EM reconstruction, device resident:
+    f <- f R#(g / max(Rf, eps)) / R# chi_C. sino: [batch x] n_theta x N float32
+    CUDA tensor (g >= 0); f0: same-batch N x N start (default: 1 inside the
+    unit disc). Returns (estimate, loglik) with loglik[b, k] the Poisson
+    log-likelihood of iterate k + 1 of slice b."""
+    import torch
+
+    g = plan.geometry
+    if not (_is_torch(sino) and sino.is_cuda and sino.dtype == torch.float32):
+        raise ValueError("expected a float32 CUDA tensor")
+    single = sino.dim() == 2
+    gb = (sino.unsqueeze(0) if single else sino).contiguous()
+    if tuple(gb.shape[1:]) != (g.n_theta, g.N):
+        raise ValueError(f"sinogram shape {tuple(sino.shape)} does not match the plan")
+    B = gb.shape[0]
+    if f0 is None:
+        f = torch.empty(B, g.N, g.N, dtype=torch.float32, device=gb.device)
+        init = 1
+    else:
+        f = (f0.unsqueeze(0) if f0.dim() == 2 else f0).to(device=gb.device, dtype=torch.float32).contiguous().clone()
+        if tuple(f.shape) != (B, g.N, g.N):
+            raise ValueError("f0 shape does not match the sinogram batch")
+        init = 0
+    ll = np.zeros((B, max(int(iters), 0)), dtype=np.float64)
+    stream = torch.cuda.current_stream(gb.device).cuda_stream
+    check(lib().lpr_gpu_em(plan.handle, gb.data_ptr(), f.data_ptr(), B, int(iters), init,
+                           ll.ctypes.data if iters > 0 else None, ctypes.c_void_p(stream)))
+    return (f[0] if single else f), (ll[0] if single else ll)
+
+
 def inner_sinogram(g: Geometry, a, b) -> float:
     """<a, b>_Sigma = 2 dtheta ds sum(a b)  (test_oracle.cpp:198-212)."""
     return float(2.0 * g.dtheta_p * g.ds * np.sum(np.asarray(a, np.float64) * np.asarray(b, np.float64)))
