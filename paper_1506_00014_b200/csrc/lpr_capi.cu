@@ -131,6 +131,9 @@ struct lpr_gpu_plan {
     float *h_in = nullptr, *h_out = nullptr;   // pinned
     cudaStream_t stream = nullptr;
     cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams
+    cudaStream_t s_aux = nullptr;                   // second half batch (run_split)
+    cudaEvent_t ev_split[3] = {};
+    bool split = false;                             // LPR_SPLIT=1: two staggered half batches (measured slower)
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     bool tex_gather = false;      // LPR_PLAN_TEXTURE_GATHER ablation
@@ -225,6 +228,9 @@ struct lpr_gpu_plan {
             if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
             if (ev_d2h[i]) cudaEventDestroy(ev_d2h[i]);
         }
+        for (auto& e : ev_split)
+            if (e) cudaEventDestroy(e);
+        if (s_aux) cudaStreamDestroy(s_aux);
         if (s_in) cudaStreamDestroy(s_in);
         if (s_out) cudaStreamDestroy(s_out);
         if (stream) cudaStreamDestroy(stream);
@@ -413,6 +419,12 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&p->s_aux, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : p->ev_split) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    {
+        const char* sp = std::getenv("LPR_SPLIT");
+        p->split = sp && sp[0] == '1';
+    }
     for (int i = 0; i < 2; ++i) {
         ck(cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming), "cudaEventCreate");
@@ -481,41 +493,77 @@ inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
     if (p->prof) ck(cudaEventRecord(p->prof[i], st), "profile event");
 }
 
-void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
+// The plan's per-slice scratch seen from slice b0 on (two concurrent half
+// batches use disjoint slices of it, run_device); `after_first`, when set, is
+// recorded after the first launch (the other half starts its chain there).
+struct Scratch {
+    Tap* q4;
+    float *qg, *fsino, *lp;
+    float2* spec;
+    DevGeom g;
+    cudaEvent_t after_first = nullptr;
+};
+
+Scratch scratch(lpr_gpu_plan* p, int b0) {
     const DevGeom& g = p->g;
+    Scratch s{};
+    s.q4 = p->q4 + size_t(b0) * g.pitch * g.pitch;
+    s.qg = p->qg + size_t(b0) * g.n_theta * g.N;
+    s.fsino = p->fsino + size_t(b0) * g.n_theta * g.N;
+    s.lp = p->lp + size_t(b0) * g.M * g.win * size_t(g.lps);
+    s.spec = p->spec + size_t(b0) * g.M * size_t(g.nts + 1) * g.n_rho;
+    s.g = g;
+    s.g.sb0 = b0;
+    return s;
+}
+
+inline void first_done(const Scratch& s, cudaStream_t st) {
+    if (s.after_first) ck(cudaEventRecord(s.after_first, st), "event");
+}
+
+void radon_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* img, float* sino, int nb, cudaStream_t st) {
+    const DevGeom& g = S.g;
     mark(p, 0, st);
-    launch_prefilter_2d(p->tex_mode == 0, nb, st, g, img, p->q4);
+    launch_prefilter_2d(p->tex_mode == 0, nb, st, g, img, S.q4);
+    first_done(S, st);
     mark(p, 1, st);
-    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->q4, p->spec, p->tex_mode);
+    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, S.q4, S.spec, p->tex_mode);
     mark(p, 2, st);
-    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_R, p->spec);
+    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_R, S.spec);
     mark(p, 3, st);
-    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->spec, p->lp);
+    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.spec, S.lp);
     mark(p, 4, st);
-    k_radon_out<<<dim3(g.n_theta, nb), 256, g.lps * sizeof(float), st>>>(g, p->lp, sino);
+    k_radon_out<<<dim3(g.n_theta, nb), 256, g.lps * sizeof(float), st>>>(g, S.lp, sino);
     mark(p, 5, st);
     check_launch("radon launch");
     p->launches += 5;
     p->ffts += 2LL * g.M * nb;
 }
+void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
+    radon_chunk_s(p, scratch(p, 0), img, sino, nb, st);
+}
 const char* const kRadonStages[] = {"prefilter_2d", "radon_theta_fwd", "rho_pass", "theta_inv", "radon_out"};
 
-void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
-    const DevGeom& g = p->g;
+void backproject_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* sino, float* img, int nb, cudaStream_t st) {
+    const DevGeom& g = S.g;
     mark(p, 0, st);
-    k_prefilter_sino_iir<<<dim3(cdiv(g.N, 256), cdiv(g.n_theta, 32), nb), 128, 0, st>>>(g, sino, p->qg);
+    k_prefilter_sino_iir<<<dim3(cdiv(g.N, 256), cdiv(g.n_theta, 32), nb), 128, 0, st>>>(g, sino, S.qg);
+    first_done(S, st);
     mark(p, 1, st);
-    launch_bp_theta_fwd(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->qg, p->spec);
+    launch_bp_theta_fwd(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.qg, S.spec);
     mark(p, 2, st);
-    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_B, p->spec);
+    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_B, S.spec);
     mark(p, 3, st);
-    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->spec, p->lp);
+    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.spec, S.lp);
     mark(p, 4, st);
-    k_bp_out<<<dim3(cdiv(g.N, 128), g.N, nb), 128, 0, st>>>(g, p->lp, img);
+    k_bp_out<<<dim3(cdiv(g.N, 128), g.N, nb), 128, 0, st>>>(g, S.lp, img);
     mark(p, 5, st);
     check_launch("backprojection launch");
     p->launches += 5;
     p->ffts += 2LL * g.M * nb;
+}
+void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
+    backproject_chunk_s(p, scratch(p, 0), sino, img, nb, st);
 }
 void transpose_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
@@ -592,15 +640,37 @@ void em_chunk(lpr_gpu_plan* p, const float* g, float* f, int nb, int iters, doub
 
 using ChunkFn = void (*)(lpr_gpu_plan*, const float*, float*, int, cudaStream_t);
 
+using ChunkSFn = void (*)(lpr_gpu_plan*, const Scratch&, const float*, float*, int, cudaStream_t);
+
+// Two half batches on two streams, the second starting once the first has
+// finished its first kernel: the halves then run different stages side by
+// side (a gather-bound theta kernel next to an FMA-bound rho pass, ...).
+void run_split(lpr_gpu_plan* p, ChunkSFn fn, const float* in, float* out, int nb, size_t in_sz, size_t out_sz,
+               cudaStream_t st) {
+    const int ha = (nb + 1) / 2, hb = nb - ha;
+    Scratch A = scratch(p, 0), B = scratch(p, ha);
+    A.after_first = p->ev_split[0];
+    ck(cudaEventRecord(p->ev_split[1], st), "event");  // B's inputs are ready when st gets here
+    fn(p, A, in, out, ha, st);
+    ck(cudaStreamWaitEvent(p->s_aux, p->ev_split[1], 0), "wait");
+    ck(cudaStreamWaitEvent(p->s_aux, p->ev_split[0], 0), "wait");
+    fn(p, B, in + size_t(ha) * in_sz, out + size_t(ha) * out_sz, hb, p->s_aux);
+    ck(cudaEventRecord(p->ev_split[2], p->s_aux), "event");
+    ck(cudaStreamWaitEvent(st, p->ev_split[2], 0), "wait");
+}
+
 void run_device(lpr_gpu_plan* p, ChunkFn fn, const float* in, float* out, int batch, size_t in_sz, size_t out_sz,
-                void* stream) {
+                void* stream, ChunkSFn sfn = nullptr) {
     if (!p) throw std::invalid_argument("null plan");
     if (batch < 0 || (batch > 0 && (!in || !out))) throw std::invalid_argument("bad buffers or batch");
     ck(cudaSetDevice(p->device), "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     for (int b0 = 0; b0 < batch; b0 += p->max_batch) {
         const int nb = std::min(p->max_batch, batch - b0);
-        fn(p, in + size_t(b0) * in_sz, out + size_t(b0) * out_sz, nb, st);
+        if (sfn && p->split && nb >= 2 && !p->prof)
+            run_split(p, sfn, in + size_t(b0) * in_sz, out + size_t(b0) * out_sz, nb, in_sz, out_sz, st);
+        else
+            fn(p, in + size_t(b0) * in_sz, out + size_t(b0) * out_sz, nb, st);
     }
 }
 
@@ -825,14 +895,14 @@ int lpr_gpu_em_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batc
 int lpr_gpu_radon(lpr_gpu_plan* p, const float* d_img, float* d_sino, int batch, void* stream) {
     return guard([&] {
         run_device(p, radon_chunk, d_img, d_sino, batch, size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0),
-                   size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0), stream);
+                   size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0), stream, radon_chunk_s);
     });
 }
 
 int lpr_gpu_backproject(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, void* stream) {
     return guard([&] {
         run_device(p, backproject_chunk, d_sino, d_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
-                   size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream);
+                   size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream, backproject_chunk_s);
     });
 }
 

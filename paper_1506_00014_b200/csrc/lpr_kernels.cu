@@ -469,7 +469,7 @@ __device__ __forceinline__ float gather_tex(const DevGeom& g, const FineRow& r, 
     const float gc0 = wc[0] + wc[1], gc1 = wc[2] + wc[3], gr0 = wr[0] + wr[1], gr1 = wr[2] + wr[3];
     const float x0 = kc + float(kApron - 1) + __fdividef(wc[1], gc0) + 0.5f;
     const float x1 = kc + float(kApron + 1) + __fdividef(wc[3], gc1) + 0.5f;
-    const float yb = float(b * g.pitch) + kr + 0.5f;
+    const float yb = float((b + g.sb0) * g.pitch) + kr + 0.5f;
     const float y0 = yb + float(kApron - 1) + __fdividef(wr[1], gr0);
     const float y1 = yb + float(kApron + 1) + __fdividef(wr[3], gr1);
     const float top = fmaf(gc0, tex2D<float>(g.qtex, x0, y0), gc1 * tex2D<float>(g.qtex, x1, y0));
@@ -490,7 +490,7 @@ __device__ __forceinline__ float gather_tld4(const DevGeom& g, const FineRow& r,
     bsw(tr - kr, wr);
     // tld4 at (x, y) returns texels (x0, y1), (x1, y1), (x1, y0), (x0, y0) with x0 = floor(x - 1/2)
     const float x0 = kc + float(kApron), x1 = x0 + 2.f;  // columns kc-1, kc | kc+1, kc+2
-    const float yb = float(b * g.pitch) + kr + float(kApron);
+    const float yb = float((b + g.sb0) * g.pitch) + kr + float(kApron);
     const float4 a = tex2Dgather<float4>(g.qtex, x0, yb, 0);        // rows kr-1, kr
     const float4 c = tex2Dgather<float4>(g.qtex, x1, yb, 0);
     const float4 d = tex2Dgather<float4>(g.qtex, x0, yb + 2.f, 0);  // rows kr+1, kr+2
@@ -995,7 +995,7 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         float sacc = 0.f;
         if (g.lptex) {  // four tld4 gathers (2 x 2 texels each, exact fp32)
             const float x0 = float(c0 + 1), x1 = x0 + 2.f;
-            const float y0 = float((b * g.M + m) * g.win + int(kt) - 1 - g.j0) + 1.f, y1 = y0 + 2.f;
+            const float y0 = float(((b + g.sb0) * g.M + m) * g.win + int(kt) - 1 - g.j0) + 1.f, y1 = y0 + 2.f;
             const float4 a = tex2Dgather<float4>(g.lptex, x0, y0, 0), e = tex2Dgather<float4>(g.lptex, x1, y0, 0);
             const float4 d = tex2Dgather<float4>(g.lptex, x0, y1, 0), f = tex2Dgather<float4>(g.lptex, x1, y1, 0);
             const float r0 = fmaf(wr[0], a.w, fmaf(wr[1], a.z, fmaf(wr[2], e.w, wr[3] * e.z)));

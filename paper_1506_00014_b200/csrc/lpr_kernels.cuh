@@ -54,6 +54,7 @@ struct DevGeom {
     const float* fir;         // 2 kFirHalf + 1 prefilter taps
     cudaTextureObject_t qtex; // texture-gather ablation: coefficient raster (0 unless enabled)
     cudaTextureObject_t lptex; // tld4 view of lp for k_bp_out (0 unless enabled)
+    int sb0;                   // first scratch slice of this launch (the textures span the whole scratch)
 };
 
 // FFT kernel variants: a compile-time register FFT for the hot lengths
