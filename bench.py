@@ -171,6 +171,29 @@ def ncu_traffic(stage: str, slices: int):
     return None
 
 
+def pcie_ceiling(h_img, d_img, d_sino, h_sino, nbytes_img, nbytes_sino, slices):
+    """Host<->device copy bandwidth, both directions at once (the e2e step moves
+    images in and sinograms out for R, the reverse for R#), and the e2e
+    throughput the link alone would allow: R phase max(H2D img, D2H sino) +
+    R# phase max(H2D sino, D2H img)."""
+    import torch
+
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    reps = 2
+    for _ in range(reps):
+        with torch.cuda.stream(s1):
+            d_img.copy_(h_img, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_sino.copy_(d_sino, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t) / reps
+    gbs = max(nbytes_img, nbytes_sino) / dt / 1e9
+    step = 2 * max(nbytes_img, nbytes_sino) / (gbs * 1e9)
+    return {"link_duplex_gbs": gbs, "link_bound_value": slices / step}
+
+
 # ------------------------------------------------------------------ CPU legs
 def cpu_sample(g, zeta, zeta_bp, slices: int = 1):
     """R then R# of `slices` slices through the oracle (fp64 CPU restatement,
@@ -316,6 +339,7 @@ def run_ours(args):
     e2e_s = max_over_ranks((time.perf_counter() - t) / e2e_steps)
     e2e_value = ws * B / e2e_s
     nbytes_img, nbytes_sino = B * g.N * g.N * 4, B * g.n_theta * g.N * 4
+    link = pcie_ceiling(h_img, imgs, sino, h_sino, nbytes_img, nbytes_sino, ws * B)
 
     # per-kernel durations measured live on the plan's stream; roofline of the
     # dominant kernel against the measured HBM copy bandwidth
@@ -353,7 +377,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config(args, g, ws),
             "radon_slices_per_s": ws * B / (ms_r / 1e3), "backproject_slices_per_s": ws * B / (ms_b / 1e3),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes_img + nbytes_sino,
-                    "d2h_bytes_per_step": nbytes_sino + nbytes_img},
+                    "d2h_bytes_per_step": nbytes_sino + nbytes_img, **link},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": dom["GBps"], "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["GBps"] / peak,

@@ -362,3 +362,46 @@ def test_em_parity_and_properties(lp, lpo, cuda):
     assert lpo.rel_l2(f1.cpu().numpy()[mask], fstar[mask]) <= 1e-2
     with pytest.raises(ValueError):
         lp.em_run(-sino, plan, 1)
+
+
+@pytest.mark.parametrize("M,n_theta", [(4, 0), (6, 0), (3, 200)])
+def test_parity_other_sector_counts_and_angles(lp, lpo, cuda, M, n_theta):
+    """Sector counts other than 3 and a non-default angle count (rounded up to
+    a multiple of 2M, geometry.cpp:69-98) run through the generic FFT lengths."""
+    import torch
+
+    N = 128
+    g = lp.sampling_plan(N, M, n_theta)
+    p = lpo.make_plan(N, M, n_theta)
+    assert g.n_theta == p.n_theta and g.n_rho == p.n_rho
+    z, zb = lpo.spectrum(p, 0), lpo.spectrum(p, 1)
+    plan = lp.RadonPlan(g, z, zb, max_batch=2)
+    f = _inputs(lpo, N, 2)
+    want = lpo.fast_radon(p, z, f)
+    got = lp.fast_radon(torch.tensor(f, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    wantb = lpo.fast_backprojection(p, zb, want)
+    gotb = lp.fast_backprojection(torch.tensor(want, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    for i in range(2):
+        assert lpo.rel_l2(got[i], want[i]) <= TOL
+        assert lpo.rel_l2(gotb[i], wantb[i]) <= TOL
+
+
+def test_unaligned_buffers_take_the_general_path(lp, lpo, cuda):
+    """Device buffers that are not 16-byte aligned (a view one float into its
+    storage) give the same result as aligned ones: the vectorised staging
+    paths check alignment and fall back to scalar loads."""
+    import torch
+
+    N = 256
+    g, p, z, zb, plan = _setup(lp, lpo, N)
+    f = torch.tensor(_inputs(lpo, N, 1)[0], dtype=torch.float32, device=cuda)
+    big = torch.zeros(N * N + 1, device=cuda)
+    big[1:] = f.flatten()
+    fu = big[1:].view(N, N)
+    assert fu.data_ptr() % 16 != 0
+    s_al, s_un = lp.fast_radon(f, plan), lp.fast_radon(fu, plan)
+    assert float((s_al - s_un).abs().max()) == 0.0
+    bs = torch.zeros(g.n_theta * N + 1, device=cuda)
+    bs[1:] = s_al.flatten()
+    su = bs[1:].view(g.n_theta, N)
+    assert float((lp.fast_backprojection(s_al, plan) - lp.fast_backprojection(su, plan)).abs().max()) == 0.0
