@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest.txt
-bash scripts/gpu_quick.sh "LPR_SPLIT=0" "LPR_SPLIT=1"
+timeout 900 python -m pytest tests -q -m gpu -x -k "parity or gaussian or transpose" 2>&1 | tail -3 > gpurun_out/pytest.txt
+python scripts/stage_times.py 2048 16 > gpurun_out/st_new.json
+LPR_GPU_LIB=$PWD/paper_1506_00014_b200/liblpradon_gpu_u4.so python scripts/stage_times.py 2048 16 > gpurun_out/st_u4.json

@@ -322,7 +322,10 @@ template <class F>
 __device__ __forceinline__ void load_packed_hermitian(Slots sm, const float2* __restrict__ in, int kmax,
                                                       int L, int n, int l0) {
     constexpr int P = F::kP;
-    constexpr int U = 4;  // independent 16-byte loads in flight per thread
+#ifndef LPR_HERM_U
+#define LPR_HERM_U 8
+#endif
+    constexpr int U = LPR_HERM_U;  // independent 16-byte loads in flight per thread
     const int total = kmax * P;
     const bool vec = l0 + 2 * P <= n && (n % 2) == 0 && (reinterpret_cast<uintptr_t>(in + l0) & 15) == 0;
     if (vec) {
@@ -716,7 +719,8 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
         const int r = e / P, p = e % P;
         const int l = l0b + 2 * p;
         if (l >= n) continue;
-        const float2 z = rs(p)[F::idx(wrapi(g.j0 + r, L2))];
+        const int q = g.j0 + r;  // in (-L2, L2): one conditional add instead of a modulo
+        const float2 z = rs(p)[F::idx(q < 0 ? q + L2 : q)];
         float* dst = out + size_t(r) * g.lps + l;
         if (l + 1 < n && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
             *reinterpret_cast<float2*>(dst) = z;
