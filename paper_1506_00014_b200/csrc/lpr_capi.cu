@@ -133,6 +133,7 @@ struct lpr_gpu_plan {
     cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams
     cudaStream_t s_aux = nullptr;                   // second half batch (run_split)
     cudaEvent_t ev_split[3] = {};
+    int host_chunks = 16;                           // pipeline depth of the pinned host path (LPR_HOST_CHUNKS; 4/8/16 measured 684/798/813 e2e)
     bool split = false;                             // LPR_SPLIT=1: two staggered half batches (measured slower)
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
@@ -422,6 +423,8 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     ck(cudaStreamCreateWithFlags(&p->s_aux, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : p->ev_split) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     {
+        const char* hc = std::getenv("LPR_HOST_CHUNKS");
+        if (hc && std::atoi(hc) > 0) p->host_chunks = std::atoi(hc);
         const char* sp = std::getenv("LPR_SPLIT");
         p->split = sp && sp[0] == '1';
     }
@@ -696,7 +699,7 @@ void run_host(lpr_gpu_plan* p, ChunkFn fn, const float* hin, float* hout, int ba
     cudaStream_t st = p->stream;
     if (pin_in && pin_out && batch > 1 && p->max_batch > 1) {
         // ~8 chunks: the exposed pipeline fill (first H2D) and drain (last D2H) shrink with the chunk
-        const int c = std::max(1, std::min(p->max_batch / 2, (batch + 7) / 8));
+        const int c = std::max(1, std::min(p->max_batch / 2, (batch + p->host_chunks - 1) / p->host_chunks));
         const int chunks = (batch + c - 1) / c;
         for (int i = 0; i < chunks; ++i) {
             const int slot = i & 1, b0 = i * c, nb = std::min(c, batch - b0);
