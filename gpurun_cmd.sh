@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu -x -k "parity_n2048 or gaussian or radon_and_back" 2>&1 | tail -3 > gpurun_out/pytest.txt
-python scripts/stage_times.py 2048 16 > gpurun_out/st_new.json
-LPR_GPU_LIB=$PWD/paper_1506_00014_b200/liblpradon_gpu_pad.so python scripts/stage_times.py 2048 16 > gpurun_out/st_pad.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_(prefilter|radon|rho|theta|bp)' -c 40 --csv --log-file gpurun_out/launches.csv python scripts/profile_one.py > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_(prefilter|radon|rho|theta|bp)' -s 10 -c 10 -o gpurun_out/prof_full python scripts/profile_one.py > gpurun_out/ncu_full.log 2>&1
