@@ -15,6 +15,7 @@
 #pragma once
 
 #include <memory>
+#include <vector>
 
 #include "lpradon/geometry.hpp"
 #include "lpradon/kernel.hpp"
@@ -45,5 +46,23 @@ Image fast_backprojection(const Sinogram& sino, const RadonPlan& plan);
 Image radon_transpose(const Sinogram& sino, const RadonPlan& plan);
 /// max over `trials` random pairs of |<Rf,g> - <f,R#g>| / (|f||g|).
 double adjoint_gap(const RadonPlan& plan, int trials);
+
+/// FBP filters along s and fbp = c_norm R#(filter(g)).
+enum class FilterKind { ramp, shepp_logan, cosine };
+Image fbp(const Sinogram& sino, const RadonPlan& plan, FilterKind kind = FilterKind::ramp);
+
+/// EM: the sensitivity R# chi_C, one step, and a run.
+struct EmState {
+    Image estimate;                      ///< >= 0, zero outside the unit disc
+    int iteration = 0;
+    Image sensitivity;                   ///< R# chi_C
+    std::vector<double> loglik_history;  ///< Poisson log-likelihood after each step
+};
+Image sensitivity_image(const RadonPlan& plan);
+/// f+ = f R#(g / max(Rf, eps)) / R# chi_C; appends the log-likelihood of f+.
+EmState em_step(EmState state, const Sinogram& g, const RadonPlan& plan);
+/// iters steps from f0 (default: 1 inside the unit disc); the history goes to *history when given.
+Image em_run(const Sinogram& g, const RadonPlan& plan, int iters, const Image* f0 = nullptr,
+             std::vector<double>* history = nullptr);
 
 }  // namespace lpr

@@ -115,6 +115,7 @@ int lpr_gpu_fbp_host(lpr_gpu_plan* plan, int kind, const float* h_sino, float* h
  * log-likelihood sum(g log Rf - Rf) over Rf > eps of every iterate f^1..f^iters.
  * A negative or non-finite g is LPR_ERR_ARG; a non-finite estimate LPR_ERR_CUDA. */
 int lpr_gpu_sensitivity(lpr_gpu_plan* plan, float* d_img, void* stream);
+int lpr_gpu_sensitivity_host(lpr_gpu_plan* plan, float* h_img);
 int lpr_gpu_em(lpr_gpu_plan* plan, const float* d_sino, float* d_img, int batch, int iters, int init,
                double* h_loglik, void* stream);
 int lpr_gpu_em_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int batch, int iters, int init,

@@ -58,6 +58,7 @@ EXPORTS = {
     "lpr_gpu_last_error": (ctypes.c_char_p, []),
     "lpr_gpu_spectrum_quadrature": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "lpr_gpu_sensitivity": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "lpr_gpu_sensitivity_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "lpr_gpu_em": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "lpr_gpu_em_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,

@@ -132,4 +132,62 @@ double adjoint_gap(const RadonPlan& plan, int trials) {
     return worst;
 }
 
+Image fbp(const Sinogram& sino, const RadonPlan& plan, FilterKind kind) {
+    const auto& p = plan.geom;
+    require(sino.values.rows() == std::size_t(p.N_theta) && sino.values.cols() == std::size_t(p.N),
+            "fbp: sinogram does not match the plan");
+    Image out;
+    out.grid = p.cartesian_grid();
+    out.pixels = Array2D<double>(p.N, p.N);
+    const std::vector<float> in = to_f32(sino.values);
+    std::vector<float> res(out.pixels.size());
+    check(lpr_gpu_fbp_host(plan.gpu.get(), int(kind), in.data(), res.data(), 1));
+    from_f32(res, out.pixels);
+    return out;
+}
+
+Image sensitivity_image(const RadonPlan& plan) {
+    const auto& p = plan.geom;
+    Image out;
+    out.grid = p.cartesian_grid();
+    out.pixels = Array2D<double>(p.N, p.N);
+    std::vector<float> res(out.pixels.size());
+    check(lpr_gpu_sensitivity_host(plan.gpu.get(), res.data()));
+    from_f32(res, out.pixels);
+    return out;
+}
+
+namespace {
+Image em_iterate(const Sinogram& g, const RadonPlan& plan, int iters, const Image* f0, std::vector<double>* hist) {
+    const auto& p = plan.geom;
+    require(g.values.rows() == std::size_t(p.N_theta) && g.values.cols() == std::size_t(p.N),
+            "em: sinogram does not match the plan");
+    require(iters >= 0, "em: iters must be >= 0");
+    if (f0) require(f0->pixels.rows() == std::size_t(p.N) && f0->pixels.cols() == std::size_t(p.N),
+                    "em: f0 does not match the plan");
+    Image out;
+    out.grid = p.cartesian_grid();
+    out.pixels = Array2D<double>(p.N, p.N);
+    const std::vector<float> gin = to_f32(g.values);
+    std::vector<float> f = f0 ? to_f32(f0->pixels) : std::vector<float>(out.pixels.size());
+    std::vector<double> ll(std::max(iters, 1));
+    check(lpr_gpu_em_host(plan.gpu.get(), gin.data(), f.data(), 1, iters, f0 ? 0 : 1, ll.data()));
+    from_f32(f, out.pixels);
+    if (hist) hist->insert(hist->end(), ll.begin(), ll.begin() + iters);
+    return out;
+}
+}  // namespace
+
+EmState em_step(EmState state, const Sinogram& g, const RadonPlan& plan) {
+    if (state.sensitivity.pixels.size() == 0) state.sensitivity = sensitivity_image(plan);
+    state.estimate = em_iterate(g, plan, 1, &state.estimate, &state.loglik_history);
+    ++state.iteration;
+    return state;
+}
+
+Image em_run(const Sinogram& g, const RadonPlan& plan, int iters, const Image* f0, std::vector<double>* history) {
+    if (iters == 0 && f0) return *f0;
+    return em_iterate(g, plan, iters, f0, history);
+}
+
 }  // namespace lpr

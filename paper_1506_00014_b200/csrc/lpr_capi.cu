@@ -822,6 +822,21 @@ int lpr_gpu_sensitivity(lpr_gpu_plan* p, float* d_img, void* stream) {
     });
 }
 
+int lpr_gpu_sensitivity_host(lpr_gpu_plan* p, float* h_img) {
+    return guard([&] {
+        if (!p || !h_img) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(p->device), "cudaSetDevice");
+        em_buffers(p);
+        cudaStream_t st = p->stream;
+        launch_fill(p->em_rf, size_t(p->geo.n_theta) * p->geo.N, 1.f, st);
+        backproject_chunk(p, p->em_rf, p->em_bp, 1, st);
+        check_launch("sensitivity");
+        ck(cudaMemcpyAsync(h_img, p->em_bp, sizeof(float) * size_t(p->geo.N) * p->geo.N, cudaMemcpyDeviceToHost, st),
+           "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
 int lpr_gpu_em(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, int iters, int init, double* h_loglik,
                void* stream) {
     return guard([&] {

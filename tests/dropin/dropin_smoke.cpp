@@ -5,6 +5,7 @@
 // CLI/FBP/EM callers would. Exit 0 when the SPEC
 // acceptance bars hold: fast vs direct <= 2e-2 and the
 // Algorithm-2 adjoint gap <= 2e-2.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -54,5 +55,36 @@ int main() {
     const double gap = lpr::adjoint_gap(plan, 3);
     std::printf("dropin N=%d: fast_radon vs direct_radon %.3e, fast_backprojection vs direct %.3e, adjoint gap %.3e\n",
                 N, e_r, e_b, gap);
-    return (e_r <= 2e-2 && e_b <= 2e-2 && gap <= 2e-2) ? 0 : 1;
+    // callers of the operators: FBP of a disc's analytic
+    // sinogram is ~1 inside (c_norm calibration), EM raises the
+    // log-likelihood of the direct sinogram and keeps the estimate >= 0
+    lpr::Sinogram disc;
+    disc.grid = geom.polar_grid();
+    disc.values = lpr::Array2D<double>(geom.N_theta, N);
+    for (int i = 0; i < geom.N_theta; ++i)
+        for (int j = 0; j < N; ++j) {
+            const double s = -0.5 + double(j) / N;
+            disc.values(i, j) = std::abs(s) < 0.25 ? 2.0 * std::sqrt(0.0625 - s * s) : 0.0;
+        }
+    const lpr::Image rec = lpr::fbp(disc, plan, lpr::FilterKind::ramp);
+    double mean = 0;
+    int cnt = 0;
+    for (int r = 0; r < N; ++r)
+        for (int c = 0; c < N; ++c) {
+            const double x = -0.5 + double(c) / N, y = -0.5 + double(r) / N;
+            if (x * x + y * y < 0.04) mean += rec.pixels(r, c), ++cnt;
+        }
+    mean /= cnt;
+    lpr::Sinogram g = direct;
+    for (auto& v : g.values.storage()) v = std::max(v, 0.0);
+    lpr::EmState st;
+    st.estimate = lpr::sensitivity_image(plan);  // any positive start
+    for (auto& v : st.estimate.pixels.storage()) v = v > 0 ? 1.0 : 0.0;
+    for (int k = 0; k < 5; ++k) st = lpr::em_step(st, g, plan);
+    double fmin = 0;
+    for (double v : st.estimate.pixels.storage()) fmin = std::min(fmin, v);
+    const bool climbs = st.loglik_history.size() == 5 && st.loglik_history.back() > st.loglik_history.front();
+    std::printf("dropin fbp disc interior mean %.4f, em loglik %.6g -> %.6g, min estimate %.3g\n", mean,
+                st.loglik_history.front(), st.loglik_history.back(), fmin);
+    return (e_r <= 2e-2 && e_b <= 2e-2 && gap <= 2e-2 && std::abs(mean - 1.0) <= 0.05 && climbs && fmin >= 0) ? 0 : 1;
 }
