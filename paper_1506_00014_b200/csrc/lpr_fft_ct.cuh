@@ -393,8 +393,13 @@ struct RhoStream {
     static constexpr int kElems = (ct_pad<S>(N - 1) + 2) / 2 * 2;  // even: every buffer starts 16-byte aligned
     // forward (R1, R2, R3 + fused) then inverse (R2, R1 to global); the whole
     // per-row convolution on a buffer whose row has landed
-    __device__ __forceinline__ static void convolve(float2* x, const float4* twf, const float4* twi, const float2* ms,
+    __device__ __forceinline__ static void convolve(float2* x, const float4* twf4, const float4* twi4, const float2* ms,
                                                     float2* out, int tid) {
+#if LPR_RHO_TW_TABLE
+        const float4 *twf = twf4, *twi = twi4;
+#else
+        const TwSincos *twf = nullptr, *twi = nullptr;
+#endif
         ct_pass<N, T, S, R1, 1, 0, false>(x, twf, tid);
         ct_pass<N, T, S, R2, R1, 0, false>(x, twf, tid);
         ct_mid_fused<N, T, S, R3, R1 * (R2 - 1)>(x, twf, ms, tid);
@@ -481,10 +486,11 @@ using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16,
 using Fft8192Band = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 // streamed rho pass for N_rho = 4374 (2 rows in flight per block, 2 blocks per SM)
-#ifndef LPR_RHO_RADIX27
-using Rho4374 = RhoStream4<4374, 512, 0, 9, 9, 9, 6>;
-#else
+// (radix 27,27,6 at 192 threads: 1.44 ms / 16 slices; 9,9,9,6 at 512 threads: 1.49)
+#ifndef LPR_RHO_RADIX9
 using Rho4374 = RhoStream<4374, 192, 0, 27, 27, 6>;
+#else
+using Rho4374 = RhoStream4<4374, 512, 0, 9, 9, 9, 6>;
 #endif
 
 }  // namespace lpr
