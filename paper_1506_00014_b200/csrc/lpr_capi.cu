@@ -126,6 +126,8 @@ struct lpr_gpu_plan {
     int band_h = 0;
     float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
     Tap* q4 = nullptr;  // coefficient raster read by the R gather; qf aliases it as the R^T scatter target
+    Tap* q4t = nullptr; // transposed quad raster for sector 0 (LPR_Q4T=0: none)
+    bool q4t_on = true;
     float2* spec = nullptr;
     float *d_in = nullptr, *d_out = nullptr;   // staging for the *_host entry points
     float *h_in = nullptr, *h_out = nullptr;   // pinned
@@ -407,6 +409,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     const size_t B = size_t(p->max_batch);
     p->tmp = p->dalloc<float>(B * G.N * g.pitch);
     p->q4 = p->dalloc<Tap>(B * g.pitch * g.pitch);
+    if (p->q4t_on && p->tex_mode == 0) p->q4t = p->dalloc<Tap>(B * g.pitch * g.pitch);
     p->qf = reinterpret_cast<float*>(p->q4);
     p->qg = p->dalloc<float>(B * G.n_theta * G.N);
     p->fsino = p->dalloc<float>(B * G.n_theta * G.N);
@@ -500,7 +503,7 @@ inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
 // batches use disjoint slices of it, run_device); `after_first`, when set, is
 // recorded after the first launch (the other half starts its chain there).
 struct Scratch {
-    Tap* q4;
+    Tap *q4, *q4t;
     float *qg, *fsino, *lp;
     float2* spec;
     DevGeom g;
@@ -511,6 +514,7 @@ Scratch scratch(lpr_gpu_plan* p, int b0) {
     const DevGeom& g = p->g;
     Scratch s{};
     s.q4 = p->q4 + size_t(b0) * g.pitch * g.pitch;
+    s.q4t = p->q4t ? p->q4t + size_t(b0) * g.pitch * g.pitch : nullptr;
     s.qg = p->qg + size_t(b0) * g.n_theta * g.N;
     s.fsino = p->fsino + size_t(b0) * g.n_theta * g.N;
     s.lp = p->lp + size_t(b0) * g.M * g.win * size_t(g.lps);
@@ -527,10 +531,11 @@ inline void first_done(const Scratch& s, cudaStream_t st) {
 void radon_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* img, float* sino, int nb, cudaStream_t st) {
     const DevGeom& g = S.g;
     mark(p, 0, st);
-    launch_prefilter_2d(p->tex_mode == 0, nb, st, g, img, S.q4);
+    launch_prefilter_2d(p->tex_mode == 0, nb, st, g, img, S.q4, S.q4t);
     first_done(S, st);
     mark(p, 1, st);
-    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, S.q4, S.spec, p->tex_mode);
+    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, S.q4, S.q4t, S.spec,
+                           p->tex_mode);
     mark(p, 2, st);
     launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_R, S.spec);
     mark(p, 3, st);
@@ -798,6 +803,8 @@ int lpr_gpu_plan_create_ex(int device, const lpr_geometry* geom, const double* z
         // LPR_TEX_TAPS=1: exact-tap tld4 texture gather (experiment; same numerics as the quad taps)
         const char* tt = std::getenv("LPR_TEX_TAPS");
         p->tex_mode = p->tex_gather ? 1 : (tt && tt[0] == '1' ? 2 : 0);
+        const char* qt = std::getenv("LPR_Q4T");
+        p->q4t_on = !(qt && qt[0] == '0');
         try {
             init_plan(p, zeta, zeta_bp);
         } catch (...) {

@@ -93,7 +93,8 @@ __device__ __forceinline__ void stage_rows(float* s, const float* __restrict__ s
 }
 
 template <class T>
-__global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float* __restrict__ img, T* __restrict__ q4) {
+__global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float* __restrict__ img, T* __restrict__ q4,
+                                                          T* __restrict__ q4t) {
     __shared__ float s[kIR][kICP];
     constexpr float z = -0.26794919243112270647f;
     constexpr float c0 = 6.0f / (1.0f - z), ca = -z / (1.0f - z);
@@ -138,24 +139,33 @@ __global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float
         const int i = idx / kIT, j = idx % kIT;
         if (y0 + i >= pitch || x0 + j >= pitch) continue;
         const float* r = s[kIW + i] + kIW + j;
-        if constexpr (sizeof(T) == 2 * sizeof(float4)) {  // octo: this row's quad and the next row's
-            const float* r2 = r + kICP;
-            dst[size_t(y0 + i) * pitch + x0 + j] = T{make_float4(r[0], r[1], r[2], r[3]), make_float4(r2[0], r2[1], r2[2], r2[3])};
-        } else if constexpr (sizeof(T) == sizeof(float4)) {
+        if constexpr (sizeof(T) == sizeof(float4)) {
             dst[size_t(y0 + i) * pitch + x0 + j] = make_float4(r[0], r[1], r[2], r[3]);
         } else {
             dst[size_t(y0 + i) * pitch + x0 + j] = r[0];
         }
     }
+    if constexpr (sizeof(T) == sizeof(float4)) {
+        if (q4t) {  // transposed quads qt[c][r] = Q[r..r+3][c] (read by sector 0); a warp writes 32 consecutive r
+            T* dt = q4t + size_t(b) * pitch * pitch;
+            for (int idx = tid; idx < kIT * kIT; idx += blockDim.x) {
+                const int i = idx % kIT, j = idx / kIT;
+                if (y0 + i >= pitch || x0 + j >= pitch) continue;
+                const float* r = s[kIW + i] + kIW + j;
+                dt[size_t(x0 + j) * pitch + y0 + i] = make_float4(r[0], r[kICP], r[2 * kICP], r[3 * kICP]);
+            }
+        }
+    }
 }
 
 // quad = false writes the plain fp32 coefficient raster (the texture ablation binds it).
-void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out) {
+void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out,
+                         void* out_t) {
     const dim3 grid((g.pitch + kIT - 1) / kIT, (g.pitch + kIT - 1) / kIT, nb);
     if (quad)
-        k_prefilter_2d_iir<Tap><<<grid, 128, 0, st>>>(g, img, static_cast<Tap*>(out));
+        k_prefilter_2d_iir<Tap><<<grid, 128, 0, st>>>(g, img, static_cast<Tap*>(out), static_cast<Tap*>(out_t));
     else
-        k_prefilter_2d_iir<float><<<grid, 128, 0, st>>>(g, img, static_cast<float*>(out));
+        k_prefilter_2d_iir<float><<<grid, 128, 0, st>>>(g, img, static_cast<float*>(out), nullptr);
 }
 
 // Recursive prefilter along s for R# (Alg. 2 step 1): a 32-row x 256-column
@@ -378,44 +388,27 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
     return true;
 }
 
-#if LPR_TAPS == 8
-// One 32-byte read-only load (LDG.256, sm_100): two tap rows of 4 coefficients.
-__device__ __forceinline__ void ldg_octo(const Octo* p, float4& a, float4& b) {
-    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
-        : "l"(p));
-}
-#endif
-
+// Cubic spline of the prefiltered image at one fine-grid point. The taps come
+// from a quad raster: element [a][b] holds Q at four consecutive b. For
+// sector 0 (`transposed`) the fine-row arcs run down image columns, so the
+// raster is the transposed one (element [c][r] = Q[r..r+3][c]) and a warp's
+// 32 consecutive samples again walk along raster rows.
 __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __restrict__ q4, const FineRow& r,
-                                              float vc, float vr, float er) {
+                                              float vc, float vr, float er, bool transposed = false) {
     float tc, tr;
     if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
-    const float kc = floorf(tc), kr = floorf(tr);
-    float wc[4], wr[4];
-    bsw(tc - kc, wc);
-    bsw(tr - kr, wr);
-    const Tap* p = q4 + (int(kr) - 1 + kApron) * g.pitch + (int(kc) - 1 + kApron);
+    const float ta = transposed ? tc : tr, tb = transposed ? tr : tc;  // raster-row and quad axes
+    const float ka = floorf(ta), kb = floorf(tb);
+    float wa[4], wb[4];
+    bsw(ta - ka, wa);
+    bsw(tb - kb, wb);
+    const Tap* p = q4 + (int(ka) - 1 + kApron) * g.pitch + (int(kb) - 1 + kApron);
     float acc = 0.f;
-#if LPR_TAPS == 8
-    float4 t[4];
-    ldg_octo(p, t[0], t[1]);                // tap rows kr-1, kr
-    ldg_octo(p + 2 * g.pitch, t[2], t[3]);  // tap rows kr+1, kr+2
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-        acc = fmaf(wr[a], fmaf(wc[0], t[a].x, fmaf(wc[1], t[a].y, fmaf(wc[2], t[a].z, wc[3] * t[a].w))), acc);
-#else
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-#if LPR_TAPS == 4
         const float4 t = __ldg(p + a * g.pitch);
-#else
-        const float* q1 = p + a * g.pitch;
-        const float4 t = make_float4(__ldg(q1), __ldg(q1 + 1), __ldg(q1 + 2), __ldg(q1 + 3));
-#endif
-        acc = fmaf(wr[a], fmaf(wc[0], t.x, fmaf(wc[1], t.y, fmaf(wc[2], t.z, wc[3] * t.w))), acc);
+        acc = fmaf(wa[a], fmaf(wb[0], t.x, fmaf(wb[1], t.y, fmaf(wb[2], t.z, wb[3] * t.w))), acc);
     }
-#endif
     return er * acc;
 }
 
@@ -511,7 +504,8 @@ __device__ __forceinline__ float gather_tld4(const DevGeom& g, const FineRow& r,
 // in flight) to hide the L2 latency of the spline taps.
 template <class F, int TEX = 0>
 __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
-                                            const Tap* __restrict__ qf, float2* __restrict__ spec) {
+                                            const Tap* __restrict__ qf, const Tap* __restrict__ qft,
+                                            float2* __restrict__ spec) {
     extern __shared__ float2 smem[];
     const Group<F> G;
     const int E = F::elems(fd);
@@ -523,7 +517,8 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
 #endif
     const int l0b = 2 * F::kP * blockIdx.x, l0 = l0b + 2 * G.g;
     const int Lf = g.Lf, nf = g.nf;
-    const Tap* q = qf + size_t(b) * g.pitch * g.pitch;
+    const bool tq = m == 0 && qft != nullptr;  // sector 0 reads the transposed raster
+    const Tap* q = (tq ? qft : qf) + size_t(b) * g.pitch * g.pitch;
     const float cm = g.cosm[m], smm = g.sinm[m], vc = g.vcm[m], vr = g.vrm[m];
     const bool one = l0 < g.n_rho, two = l0 + 1 < g.n_rho;
     const float er0 = one ? __ldg(g.erho + l0) : 0.f;
@@ -542,8 +537,8 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
                     return make_float2(one ? gather_tld4(g, fr, vc, vr, er0, b) : 0.f,
                                        two ? gather_tld4(g, fr, vc, vr, er1, b) : 0.f);
                 else
-                    return make_float2(one ? gather_image(g, q, fr, vc, vr, er0) : 0.f,
-                                       two ? gather_image(g, q, fr, vc, vr, er1) : 0.f);
+                    return make_float2(one ? gather_image(g, q, fr, vc, vr, er0, tq) : 0.f,
+                                       two ? gather_image(g, q, fr, vc, vr, er1, tq) : 0.f);
             });
 #ifndef LPR_EXP_NOFFT  // timing experiment only: skip the FFT passes after the gathered first pass
             F::template run_tail<false>(sm, fd, G.tid);
@@ -577,10 +572,10 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
             h2 = one ? gather_tex(g, r2, vc, vr, er0, b) : 0.f;
             h3 = two ? gather_tex(g, r2, vc, vr, er1, b) : 0.f;
         } else {
-            h0 = one ? gather_image(g, q, r1, vc, vr, er0) : 0.f;
-            h1 = two ? gather_image(g, q, r1, vc, vr, er1) : 0.f;
-            h2 = one ? gather_image(g, q, r2, vc, vr, er0) : 0.f;
-            h3 = two ? gather_image(g, q, r2, vc, vr, er1) : 0.f;
+            h0 = one ? gather_image(g, q, r1, vc, vr, er0, tq) : 0.f;
+            h1 = two ? gather_image(g, q, r1, vc, vr, er1, tq) : 0.f;
+            h2 = one ? gather_image(g, q, r2, vc, vr, er0, tq) : 0.f;
+            h3 = two ? gather_image(g, q, r2, vc, vr, er1, tq) : 0.f;
         }
         sm[F::idx(i - nf / 2 + Lf)] = make_float2(h0, h1);  // q = i - nf/2 < 0
         sm[F::idx(i2 - nf / 2)] = make_float2(h2, h3);      // q = i2 - nf/2 >= 0
@@ -1113,20 +1108,20 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 }
 
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const Tap* qf, float2* spec, int tex) {
+                            const Tap* qf, const Tap* qft, float2* spec, int tex) {
     if (tex == 1) {
-#define CALL(F) k_radon_theta_fwd<F, 1><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
+#define CALL(F) k_radon_theta_fwd<F, 1><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
         LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
         return;
     }
     if (tex == 2) {
-#define CALL(F) k_radon_theta_fwd<F, 2><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
+#define CALL(F) k_radon_theta_fwd<F, 2><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
         LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
         return;
     }
-#define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, spec)
+#define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
     if (L.variant == kFft8192) {
         CALL(Fft8192Band);
         return;

@@ -12,23 +12,10 @@ namespace lpr {
 
 constexpr int kMaxSectors = 16;
 
-// Layout of the image B-spline coefficients read by the fine-grid gather:
-// LPR_TAPS 8 = octo taps (element [r][c] = Q[r][c..c+3] and Q[r+1][c..c+3],
-// 32 bytes: two spline tap rows per LDG.256, so a sample is 2 loads),
-// 4 = quad taps (one 16-byte load per tap row), 1 = plain fp32 raster.
-#ifndef LPR_TAPS
-#define LPR_TAPS 4
-#endif
-struct __align__(32) Octo {
-    float4 lo, hi;
-};
-#if LPR_TAPS == 8
-using Tap = Octo;
-#elif LPR_TAPS == 4
+// The image B-spline coefficients read by the fine-grid gather: quad taps,
+// element [r][c] = Q[r][c..c+3] (one 16-byte load per spline tap row), plus
+// the transposed raster for sector 0 (element [c][r] = Q[r..r+3][c]).
 using Tap = float4;
-#else
-using Tap = float;
-#endif
 constexpr int kApron = 4;     // mirrored border around the image coefficients
 constexpr int kFirHalf = 16;  // B-spline prefilter impulse-response half length
 
@@ -75,8 +62,9 @@ std::vector<float2> fft_pass_twiddles(int variant);
 cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
                                 size_t rho_mult_bytes);
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const Tap* qf, float2* spec, int tex);  // tex: 0 soft taps, 1 hw bilinear, 2 tld4 exact taps
-void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out);
+                            const Tap* qf, const Tap* qft, float2* spec, int tex);  // tex: 0 soft taps, 1 hw bilinear, 2 tld4 exact taps
+void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out,
+                         void* out_t);
 size_t rho_stream_smem(int variant);  // 0: no streamed rho kernel for this length
 std::vector<float4> rho_stream_inv_twiddles(int variant);
 std::vector<float4> rho_stream_fwd_twiddles(int variant);

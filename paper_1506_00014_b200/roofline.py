@@ -22,8 +22,9 @@ def stage_bytes(g, op: str, batch: int) -> dict:
     S = nt * N
     if op == "radon":
         per = {
-            "prefilter_2d": 4 * P + 16 * pitch * pitch,
-            "radon_theta_fwd": 16 * pitch * pitch + 8 * M * H,
+            # quad raster + its transpose (sector 0 reads the transposed one)
+            "prefilter_2d": 4 * P + 32 * pitch * pitch,
+            "radon_theta_fwd": 32 * pitch * pitch + 8 * M * H,
             "rho_pass": 16 * M * H,
             "theta_inv": 8 * M * H + 4 * M * W,
             "radon_out": 4 * M * nts * nr + 4 * S,
