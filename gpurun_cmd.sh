@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_trun.json 2> gpurun_out/bench_trun.err
-timeout 300 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -2 > gpurun_out/pytest.txt
+python scripts/stage_times.py 2048 16 > gpurun_out/st_new.json

@@ -45,6 +45,19 @@ __device__ __forceinline__ void bsw(float a, float w[4]) {
     w[3] = a2 * a * (1.0f / 6.0f);
 }
 
+// Both axes' tap weights at once on the packed fp32x2 pipe: (wx[k], wy[k]) = bsw
+// of (ax, ay), the same polynomials as bsw.
+__device__ __forceinline__ void bsw2(float2 a, float2 w[4]) {
+    const float2 b = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-a.x, -a.y));
+    const float2 a2 = __fmul2_rn(a, a), b2 = __fmul2_rn(b, b);
+    const float2 sixth = make_float2(1.0f / 6.0f, 1.0f / 6.0f), half = make_float2(0.5f, 0.5f);
+    const float2 m1 = make_float2(-1.f, -1.f), two3 = make_float2(2.0f / 3.0f, 2.0f / 3.0f);
+    w[0] = __fmul2_rn(__fmul2_rn(b2, b), sixth);
+    w[1] = __ffma2_rn(a2, __ffma2_rn(half, a, m1), two3);
+    w[2] = __ffma2_rn(b2, __ffma2_rn(half, b, m1), two3);
+    w[3] = __fmul2_rn(__fmul2_rn(a2, a), sixth);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------- prefilter
@@ -399,15 +412,14 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __res
     if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
     const float ta = transposed ? tc : tr, tb = transposed ? tr : tc;  // raster-row and quad axes
     const float ka = floorf(ta), kb = floorf(tb);
-    float wa[4], wb[4];
-    bsw(ta - ka, wa);
-    bsw(tb - kb, wb);
+    float2 w[4];  // (row-axis, quad-axis) weights
+    bsw2(make_float2(ta - ka, tb - kb), w);
     const Tap* p = q4 + (int(ka) - 1 + kApron) * g.pitch + (int(kb) - 1 + kApron);
     float acc = 0.f;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const float4 t = __ldg(p + a * g.pitch);
-        acc = fmaf(wa[a], fmaf(wb[0], t.x, fmaf(wb[1], t.y, fmaf(wb[2], t.z, wb[3] * t.w))), acc);
+        acc = fmaf(w[a].x, fmaf(w[0].y, t.x, fmaf(w[1].y, t.y, fmaf(w[2].y, t.z, w[3].y * t.w))), acc);
     }
     return er * acc;
 }
@@ -987,8 +999,15 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         const float tr = (rho - g.log_ar) * g.inv_drho;
         const float kt = floorf(tt), kr = floorf(tr);
         float wt[4], wr[4];
-        bsw(tt - kt, wt);
-        bsw(tr - kr, wr);
+        {
+            float2 w2[4];
+            bsw2(make_float2(tt - kt, tr - kr), w2);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                wt[q] = w2[q].x;
+                wr[q] = w2[q].y;
+            }
+        }
         const float* base = lp + (size_t(b) * g.M + m) * size_t(g.win) * g.lps + (int(kt) - 1 - g.j0) * g.lps;
         const int c0 = int(kr) - 1;
         float sacc = 0.f;
