@@ -303,6 +303,17 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     g.fir = p->upload(fir);
 
     p->build_desc(g.Lf, p->d_fine, p->l_fine);
+    {  // row rotations of the fused fine first pass (k_radon_theta_fwd)
+        const int r1 = fft_first_radix(p->l_fine.variant);
+        g.fine_b1 = 0;
+        if (r1 > 0 && g.Lf % r1 == 0 && r1 / 2 <= 16) {
+            g.fine_b1 = g.Lf / r1;
+            for (int j = 0; j < 16; ++j) {
+                const double a = double(j) * g.fine_b1 * G.dtheta_lp;
+                g.fine_rot[j] = make_float2(float(std::cos(a)), float(std::sin(a)));
+            }
+        }
+    }
     p->build_desc(G.n_rho, p->d_rho, p->l_rho, true);
     p->build_desc(g.L2, p->d_coarse, p->l_coarse);
     p->build_desc(2L * G.N, p->d_filt, p->l_filt);

@@ -443,10 +443,11 @@ __device__ __forceinline__ void first_pass_gathered(float2* sm, int tid, Gather&
             float2 v[R1];
 #pragma unroll
             for (int r = 0; r < R1; ++r) {
+                // gathered rows are bb + B1 j, j = 0 .. R1/2 - 1
                 if (r < R1 / 4) {
-                    v[r] = gather(bb + B1 * r + N / 4);  // p in [0, N/4)
+                    v[r] = gather(bb + B1 * r + N / 4, r + R1 / 4);  // p in [0, N/4)
                 } else if (r >= 3 * R1 / 4) {
-                    v[r] = gather(bb + B1 * r - 3 * N / 4);  // p in [3N/4, N)
+                    v[r] = gather(bb + B1 * r - 3 * N / 4, r - 3 * R1 / 4);  // p in [3N/4, N)
                 } else {
                     v[r] = make_float2(0.f, 0.f);
                 }
@@ -537,11 +538,25 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
     const float er1 = two ? __ldg(g.erho + l0 + 1) : 0.f;
     if constexpr (kFusedFirstPass<F>) {
         if (F::kN == Lf) {
-            first_pass_gathered<F>(sm, G.tid, [&](int row) {
+            // the thread's rows are bb + B1 j: (cos, sin) of row bb from the table,
+            // the others by an exact-to-fp32 rotation by j B1 dtheta_lp (no dependent load per row)
+            constexpr int B1 = F::kN / F::kR1;
+            const bool rot = B1 <= F::kT && g.fine_b1 == B1;  // one butterfly per thread: bb = G.tid
+            const float cb = __ldg(g.fine_cos + G.tid), sb = __ldg(g.fine_sin + G.tid);
+            first_pass_gathered<F>(sm, G.tid, [&](int row, int j) {
 #ifdef LPR_EXP_NOGATHER  // timing experiment only: no image taps
                 return make_float2(er0 * row, er1 * row);
 #endif
-                const FineRow fr = fine_row(g, cm, smm, __ldg(g.fine_cos + row), __ldg(g.fine_sin + row));
+                float ct, st;
+                if (rot) {
+                    const float2 w = g.fine_rot[j];
+                    ct = fmaf(cb, w.x, -sb * w.y);
+                    st = fmaf(sb, w.x, cb * w.y);
+                } else {
+                    ct = __ldg(g.fine_cos + row);
+                    st = __ldg(g.fine_sin + row);
+                }
+                const FineRow fr = fine_row(g, cm, smm, ct, st);
                 if constexpr (TEX == 1)
                     return make_float2(one ? gather_tex(g, fr, vc, vr, er0, b) : 0.f,
                                        two ? gather_tex(g, fr, vc, vr, er1, b) : 0.f);
@@ -818,7 +833,7 @@ __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, cons
     const float halfN = 0.5f * N;
     if constexpr (kFusedFirstPass<F>) {
         if (F::kN == L2) {
-            first_pass_gathered<F>(sm, G.tid, [&](int jj) {
+            first_pass_gathered<F>(sm, G.tid, [&](int jj, int) {
                 const int j = jj - nts / 2;
                 int i = m * nts + j;
                 const bool flip = i < 0;
@@ -1057,6 +1072,17 @@ std::vector<float2> fft_pass_twiddles(int variant) {
         case kFft8192: return Fft8192::pass_twiddles();
         case kFft16384: return Fft16384::pass_twiddles();
         default: return {};
+    }
+}
+
+int fft_first_radix(int variant) {
+    switch (variant) {
+        case kFft2048: return Fft2048::kR1;
+        case kFft4096: return Fft4096::kR1;
+        case kFft4374: return Fft4374::kR1;
+        case kFft8192: return Fft8192::kR1;
+        case kFft16384: return Fft16384::kR1;
+        default: return 0;
     }
 }
 

@@ -36,6 +36,8 @@ struct DevGeom {
     // tables (device)
     const float* fine_cos;    // nf entries: cos(q dtheta_lp), q = i - nf/2
     const float* fine_sin;
+    int fine_b1;              // stride of a thread's rows in the fused fine first pass (0: use the tables)
+    float2 fine_rot[16];      // (cos, sin)(j fine_b1 dtheta_lp), j < 16
     const float* coarse_cos;  // nts entries: cos(j dtheta_p), j = jj - nts/2
     const float* erho;        // n_rho entries: exp(log a_r + l drho)
     const float* fir;         // 2 kFirHalf + 1 prefilter taps
@@ -58,6 +60,7 @@ struct FftLaunch {
 
 // host-side launchers (lpr_kernels.cu)
 FftLaunch fft_launch_config(const FftDesc& d);
+int fft_first_radix(int variant);  // 0 for the generic plan
 std::vector<float2> fft_pass_twiddles(int variant);
 cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
                                 size_t rho_mult_bytes);
