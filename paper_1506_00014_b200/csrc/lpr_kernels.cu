@@ -406,19 +406,23 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
 // sector 0 (`transposed`) the fine-row arcs run down image columns, so the
 // raster is the transposed one (element [c][r] = Q[r..r+3][c]) and a warp's
 // 32 consecutive samples again walk along raster rows.
+constexpr int kPitch2048 = 2048 + 2 * kApron;  // raster pitch of the N = 2048 plans (the bench size)
+
+template <int PITCH = 0>  // compile-time raster pitch (0: g.pitch): the tap-row offsets become load immediates
 __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __restrict__ q4, const FineRow& r,
                                               float vc, float vr, float er, bool transposed = false) {
+    const int pitch = PITCH ? PITCH : g.pitch;
     float tc, tr;
     if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
     const float ta = transposed ? tc : tr, tb = transposed ? tr : tc;  // raster-row and quad axes
     const float ka = floorf(ta), kb = floorf(tb);
     float2 w[4];  // (row-axis, quad-axis) weights
     bsw2(make_float2(ta - ka, tb - kb), w);
-    const Tap* p = q4 + (int(ka) - 1 + kApron) * g.pitch + (int(kb) - 1 + kApron);
+    const Tap* p = q4 + ((int(ka) - 1 + kApron) * pitch + (int(kb) - 1 + kApron));
     float acc = 0.f;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const float4 t = __ldg(p + a * g.pitch);
+        const float4 t = __ldg(p + a * pitch);
         acc = fmaf(w[a].x, fmaf(w[0].y, t.x, fmaf(w[1].y, t.y, fmaf(w[2].y, t.z, w[3].y * t.w))), acc);
     }
     return er * acc;
@@ -515,7 +519,7 @@ __device__ __forceinline__ float gather_tld4(const DevGeom& g, const FineRow& r,
 // zero-embed into the doubled fine period Lf, real theta FFT, keep |k| < nts.
 // Each thread gathers two fine rows per iteration (64 independent tap loads
 // in flight) to hide the L2 latency of the spline taps.
-template <class F, int TEX = 0>
+template <class F, int TEX = 0, int PITCH = 0>
 __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                             const Tap* __restrict__ qf, const Tap* __restrict__ qft,
                                             float2* __restrict__ spec) {
@@ -564,8 +568,8 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
                     return make_float2(one ? gather_tld4(g, fr, vc, vr, er0, b) : 0.f,
                                        two ? gather_tld4(g, fr, vc, vr, er1, b) : 0.f);
                 else
-                    return make_float2(one ? gather_image(g, q, fr, vc, vr, er0, tq) : 0.f,
-                                       two ? gather_image(g, q, fr, vc, vr, er1, tq) : 0.f);
+                    return make_float2(one ? gather_image<PITCH>(g, q, fr, vc, vr, er0, tq) : 0.f,
+                                       two ? gather_image<PITCH>(g, q, fr, vc, vr, er1, tq) : 0.f);
             });
 #ifndef LPR_EXP_NOFFT  // timing experiment only: skip the FFT passes after the gathered first pass
             F::template run_tail<false>(sm, fd, G.tid);
@@ -1130,7 +1134,10 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
         cudaError_t r = smem_attr((const void*)K, L);                          \
         if (r != cudaSuccess) e = r;                                           \
     } while (0)
-    if (fine.variant == kFft8192) SET(k_radon_theta_fwd<Fft8192Band>, fine.smem * fine.per_block);
+    if (fine.variant == kFft8192) {
+        SET(k_radon_theta_fwd<Fft8192Band>, fine.smem * fine.per_block);
+        SET((k_radon_theta_fwd<Fft8192Band, 0, kPitch2048>), fine.smem * fine.per_block);
+    }
 #define FINE(F)                                                   \
     SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block);         \
     SET((k_radon_theta_fwd<F, 1>), fine.smem * fine.per_block);    \
@@ -1168,7 +1175,11 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
     }
 #define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
     if (L.variant == kFft8192) {
-        CALL(Fft8192Band);
+        if (g.pitch == kPitch2048)
+            k_radon_theta_fwd<Fft8192Band, 0, kPitch2048><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(
+                g, fd, qf, qft, spec);
+        else
+            CALL(Fft8192Band);
         return;
     }
     LPR_FFT_SWITCH(L.variant, CALL)
