@@ -305,7 +305,8 @@ __device__ __forceinline__ void store_half_spectra(Slots res, int L, int nts, in
 // Z(L - k) = x[L/2 - k] + conj(w) x[L - k], w = exp(-2 pi i k / L).
 template <class F>
 __device__ __forceinline__ void store_half_spectra_r2(Slots res, int L, int nts, int n_rho, int l0b,
-                                                      float2* __restrict__ out) {
+                                                      float2* __restrict__ out, float s0 = 1.f, float s1 = 1.f) {
+    const float h0 = 0.5f * s0, h1 = 0.5f * s1;  // column scales (P = 1), with the 1/2 of the split
     constexpr int P = F::kP;
     const int H = L / 2;
     for (int e = threadIdx.x; e < (nts + 1) * P; e += blockDim.x) {
@@ -320,8 +321,8 @@ __device__ __forceinline__ void store_half_spectra_r2(Slots res, int L, int nts,
             const float2* x = res(p);
             const float2 z = cadd(x[F::idx(k)], cmul(x[F::idx(k + H)], w));
             const float2 zm = k == 0 ? z : cadd(x[F::idx(H - k)], cmulc(x[F::idx(L - k)], w));
-            A = make_float2(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y));
-            B = make_float2(0.5f * (z.y + zm.y), -0.5f * (z.x - zm.x));
+            A = make_float2(h0 * (z.x + zm.x), h0 * (z.y - zm.y));
+            B = make_float2(h1 * (z.y + zm.y), -h1 * (z.x - zm.x));
         }
         float2* dst = out + size_t(k) * n_rho + l;
         if (l + 1 < n_rho && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -408,7 +409,9 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
 // 32 consecutive samples again walk along raster rows.
 constexpr int kPitch2048 = 2048 + 2 * kApron;  // raster pitch of the N = 2048 plans (the bench size)
 
-template <int PITCH = 0>  // compile-time raster pitch (0: g.pitch): the tap-row offsets become load immediates
+// SCALE = false leaves out the e^rho factor (constant along a column: the
+// fused kernel applies it to the column's spectrum instead of every sample).
+template <int PITCH = 0, bool SCALE = true>  // compile-time raster pitch (0: g.pitch): tap-row offsets as load immediates
 __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __restrict__ q4, const FineRow& r,
                                               float vc, float vr, float er, bool transposed = false) {
     const int pitch = PITCH ? PITCH : g.pitch;
@@ -425,7 +428,7 @@ __device__ __forceinline__ float gather_image(const DevGeom& g, const Tap* __res
         const float4 t = __ldg(p + a * pitch);
         acc = fmaf(w[a].x, fmaf(w[0].y, t.x, fmaf(w[1].y, t.y, fmaf(w[2].y, t.z, w[3].y * t.w))), acc);
     }
-    return er * acc;
+    return SCALE ? er * acc : acc;
 }
 
 // First FFT pass fused with the sample gather, for a real-pair transform of
@@ -544,6 +547,7 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         if (F::kN == Lf) {
             // the thread's rows are bb + B1 j: (cos, sin) of row bb from the table,
             // the others by an exact-to-fp32 rotation by j B1 dtheta_lp (no dependent load per row)
+            constexpr bool kScaleAtStore = TEX == 0 && F::kLast2 && F::kP == 1;
             constexpr int B1 = F::kN / F::kR1;
             const bool rot = B1 <= F::kT && g.fine_b1 == B1;  // one butterfly per thread: bb = G.tid
             const float cb = __ldg(g.fine_cos + G.tid), sb = __ldg(g.fine_sin + G.tid);
@@ -568,15 +572,16 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
                     return make_float2(one ? gather_tld4(g, fr, vc, vr, er0, b) : 0.f,
                                        two ? gather_tld4(g, fr, vc, vr, er1, b) : 0.f);
                 else
-                    return make_float2(one ? gather_image<PITCH>(g, q, fr, vc, vr, er0, tq) : 0.f,
-                                       two ? gather_image<PITCH>(g, q, fr, vc, vr, er1, tq) : 0.f);
+                    return make_float2(one ? gather_image<PITCH, !kScaleAtStore>(g, q, fr, vc, vr, er0, tq) : 0.f,
+                                       two ? gather_image<PITCH, !kScaleAtStore>(g, q, fr, vc, vr, er1, tq) : 0.f);
             });
 #ifndef LPR_EXP_NOFFT  // timing experiment only: skip the FFT passes after the gathered first pass
             F::template run_tail<false>(sm, fd, G.tid);
 #endif
             float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
             if constexpr (F::kLast2)
-                store_half_spectra_r2<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out);
+                store_half_spectra_r2<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out,
+                                         kScaleAtStore ? er0 : 1.f, kScaleAtStore ? er1 : 1.f);
             else
                 store_half_spectra<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out);
             return;
