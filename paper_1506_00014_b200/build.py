@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 # Experiment variants: LPR_VARIANT=name builds liblpradon_gpu_<name>.so with
-# the extra nvcc defines in LPR_DEFS (e.g. "-DLPR_TAPS=1"); the default build
+# the extra nvcc defines in LPR_DEFS (e.g. "-DLPR_RHO_RADIX9"); the default build
 # is the product library.
 _VARIANT = os.environ.get("LPR_VARIANT", "")
 BUILD = os.path.join(PKG, "_build" + (f"_{_VARIANT}" if _VARIANT else ""))

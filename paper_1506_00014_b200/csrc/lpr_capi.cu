@@ -140,7 +140,7 @@ struct lpr_gpu_plan {
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     bool tex_gather = false;      // LPR_PLAN_TEXTURE_GATHER ablation
-    int tex_mode = 0;             // gather path of the R fine grid: 0 quad taps, 1 hw bilinear, 2 tld4 exact taps
+    int tex_mode = 0;             // gather path of the R fine grid: 0 quad taps, 1 hardware bilinear (ablation)
     cudaTextureObject_t qtex = 0;
     cudaTextureObject_t lptex = 0;  // tld4 view of lp for the R# output resampling (LPR_BP_TEX=0: direct loads)
     std::vector<void*> allocs;
@@ -468,7 +468,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         rd.res.pitch2D.pitchInBytes = pitch_bytes;
         cudaTextureDesc td{};
         td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
-        td.filterMode = p->tex_mode == 1 ? cudaFilterModeLinear : cudaFilterModePoint;
+        td.filterMode = cudaFilterModeLinear;
         td.readMode = cudaReadModeElementType;
         td.normalizedCoords = 0;
         ck(cudaCreateTextureObject(&p->qtex, &rd, &td, nullptr), "cudaCreateTextureObject");
@@ -811,9 +811,7 @@ int lpr_gpu_plan_create_ex(int device, const lpr_geometry* geom, const double* z
         p->geo = G;
         p->max_batch = max_batch;
         p->tex_gather = (flags & LPR_PLAN_TEXTURE_GATHER) != 0;
-        // LPR_TEX_TAPS=1: exact-tap tld4 texture gather (experiment; same numerics as the quad taps)
-        const char* tt = std::getenv("LPR_TEX_TAPS");
-        p->tex_mode = p->tex_gather ? 1 : (tt && tt[0] == '1' ? 2 : 0);
+        p->tex_mode = p->tex_gather ? 1 : 0;
         const char* qt = std::getenv("LPR_Q4T");
         p->q4t_on = !(qt && qt[0] == '0');
         try {

@@ -30,10 +30,6 @@ __device__ __forceinline__ int mirror_idx(int i, int n) {
     return r >= n ? per - r : r;
 }
 
-__device__ __forceinline__ int wrapi(int i, int n) {
-    int r = i % n;
-    return r < 0 ? r + n : r;
-}
 
 // Cubic B-spline taps for t = k + a: weights of samples k-1, k, k+1, k+2.
 __device__ __forceinline__ void bsw(float a, float w[4]) {
@@ -493,31 +489,6 @@ __device__ __forceinline__ float gather_tex(const DevGeom& g, const FineRow& r, 
     return er * fmaf(gr0, top, gr1 * bot);
 }
 
-// Exact-tap texture variant: the 4 x 4 spline footprint as four tld4
-// gathers (2 x 2 texels each, returned unfiltered in fp32) from the plain
-// coefficient raster, weights in fp32 as in gather_image. The texture path
-// brings the 2-D block-linear cache layout and its own fetch pipeline.
-__device__ __forceinline__ float gather_tld4(const DevGeom& g, const FineRow& r, float vc, float vr, float er, int b) {
-    float tc, tr;
-    if (!fine_pos(g, r, vc, vr, er, tc, tr)) return 0.f;
-    const float kc = floorf(tc), kr = floorf(tr);
-    float wc[4], wr[4];
-    bsw(tc - kc, wc);
-    bsw(tr - kr, wr);
-    // tld4 at (x, y) returns texels (x0, y1), (x1, y1), (x1, y0), (x0, y0) with x0 = floor(x - 1/2)
-    const float x0 = kc + float(kApron), x1 = x0 + 2.f;  // columns kc-1, kc | kc+1, kc+2
-    const float yb = float((b + g.sb0) * g.pitch) + kr + float(kApron);
-    const float4 a = tex2Dgather<float4>(g.qtex, x0, yb, 0);        // rows kr-1, kr
-    const float4 c = tex2Dgather<float4>(g.qtex, x1, yb, 0);
-    const float4 d = tex2Dgather<float4>(g.qtex, x0, yb + 2.f, 0);  // rows kr+1, kr+2
-    const float4 e = tex2Dgather<float4>(g.qtex, x1, yb + 2.f, 0);
-    const float r0 = fmaf(wc[0], a.w, fmaf(wc[1], a.z, fmaf(wc[2], c.w, wc[3] * c.z)));
-    const float r1 = fmaf(wc[0], a.x, fmaf(wc[1], a.y, fmaf(wc[2], c.x, wc[3] * c.y)));
-    const float r2 = fmaf(wc[0], d.w, fmaf(wc[1], d.z, fmaf(wc[2], e.w, wc[3] * e.z)));
-    const float r3 = fmaf(wc[0], d.x, fmaf(wc[1], d.y, fmaf(wc[2], e.x, wc[3] * e.y)));
-    return er * fmaf(wr[0], r0, fmaf(wr[1], r1, fmaf(wr[2], r2, wr[3] * r3)));
-}
-
 // Alg. 1 steps 3-6a: gather T_m f e^rho on the fine grid of two rho columns,
 // zero-embed into the doubled fine period Lf, real theta FFT, keep |k| < nts.
 // Each thread gathers two fine rows per iteration (64 independent tap loads
@@ -530,11 +501,7 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
     const Group<F> G;
     const int E = F::elems(fd);
     float2* sm = smem + G.g * E;
-#ifdef LPR_FORCE_SECTOR  // timing experiment only: every block gathers sector LPR_FORCE_SECTOR
-    const int m = LPR_FORCE_SECTOR, b = blockIdx.z;
-#else
     const int m = blockIdx.y, b = blockIdx.z;
-#endif
     const int l0b = 2 * F::kP * blockIdx.x, l0 = l0b + 2 * G.g;
     const int Lf = g.Lf, nf = g.nf;
     const bool tq = m == 0 && qft != nullptr;  // sector 0 reads the transposed raster
@@ -552,9 +519,6 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
             const bool rot = B1 <= F::kT && g.fine_b1 == B1;  // one butterfly per thread: bb = G.tid
             const float cb = __ldg(g.fine_cos + G.tid), sb = __ldg(g.fine_sin + G.tid);
             first_pass_gathered<F>(sm, G.tid, [&](int row, int j) {
-#ifdef LPR_EXP_NOGATHER  // timing experiment only: no image taps
-                return make_float2(er0 * row, er1 * row);
-#endif
                 float ct, st;
                 if (rot) {
                     const float2 w = g.fine_rot[j];
@@ -568,16 +532,11 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
                 if constexpr (TEX == 1)
                     return make_float2(one ? gather_tex(g, fr, vc, vr, er0, b) : 0.f,
                                        two ? gather_tex(g, fr, vc, vr, er1, b) : 0.f);
-                else if constexpr (TEX == 2)
-                    return make_float2(one ? gather_tld4(g, fr, vc, vr, er0, b) : 0.f,
-                                       two ? gather_tld4(g, fr, vc, vr, er1, b) : 0.f);
                 else
                     return make_float2(one ? gather_image<PITCH, !kScaleAtStore>(g, q, fr, vc, vr, er0, tq) : 0.f,
                                        two ? gather_image<PITCH, !kScaleAtStore>(g, q, fr, vc, vr, er1, tq) : 0.f);
             });
-#ifndef LPR_EXP_NOFFT  // timing experiment only: skip the FFT passes after the gathered first pass
             F::template run_tail<false>(sm, fd, G.tid);
-#endif
             float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
             if constexpr (F::kLast2)
                 store_half_spectra_r2<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out,
@@ -597,12 +556,7 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
         const FineRow r1 = fine_row(g, cm, smm, __ldg(g.fine_cos + i), __ldg(g.fine_sin + i));
         const FineRow r2 = fine_row(g, cm, smm, __ldg(g.fine_cos + i2), __ldg(g.fine_sin + i2));
         float h0, h1, h2, h3;
-        if constexpr (TEX == 2) {
-            h0 = one ? gather_tld4(g, r1, vc, vr, er0, b) : 0.f;
-            h1 = two ? gather_tld4(g, r1, vc, vr, er1, b) : 0.f;
-            h2 = one ? gather_tld4(g, r2, vc, vr, er0, b) : 0.f;
-            h3 = two ? gather_tld4(g, r2, vc, vr, er1, b) : 0.f;
-        } else if constexpr (TEX == 1) {
+        if constexpr (TEX == 1) {
             h0 = one ? gather_tex(g, r1, vc, vr, er0, b) : 0.f;
             h1 = two ? gather_tex(g, r1, vc, vr, er1, b) : 0.f;
             h2 = one ? gather_tex(g, r2, vc, vr, er0, b) : 0.f;
@@ -1146,7 +1100,6 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 #define FINE(F)                                                   \
     SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block);         \
     SET((k_radon_theta_fwd<F, 1>), fine.smem * fine.per_block);    \
-    SET((k_radon_theta_fwd<F, 2>), fine.smem * fine.per_block);    \
     SET(k_theta_inv_fine_T<F>, fine.smem * fine.per_block)
 #define RHO(F) SET(k_rho_pass<F>, rho.smem + rho_mult_bytes)
     if (rho.variant == kFft4374) SET(k_rho_stream<Rho4374>, rho_stream_smem(kFft4374));
@@ -1168,12 +1121,6 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
                             const Tap* qf, const Tap* qft, float2* spec, int tex) {
     if (tex == 1) {
 #define CALL(F) k_radon_theta_fwd<F, 1><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
-        LPR_FFT_SWITCH(L.variant, CALL)
-#undef CALL
-        return;
-    }
-    if (tex == 2) {
-#define CALL(F) k_radon_theta_fwd<F, 2><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
         LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
         return;

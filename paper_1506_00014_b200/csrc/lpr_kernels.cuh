@@ -65,7 +65,7 @@ std::vector<float2> fft_pass_twiddles(int variant);
 cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, const FftLaunch& coarse,
                                 size_t rho_mult_bytes);
 void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
-                            const Tap* qf, const Tap* qft, float2* spec, int tex);  // tex: 0 soft taps, 1 hw bilinear, 2 tld4 exact taps
+                            const Tap* qf, const Tap* qft, float2* spec, int tex);  // tex: 0 quad taps, 1 hardware bilinear (ablation)
 void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, const float* img, void* out,
                          void* out_t);
 size_t rho_stream_smem(int variant);  // 0: no streamed rho kernel for this length
