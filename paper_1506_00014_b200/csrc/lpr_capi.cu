@@ -21,6 +21,7 @@ namespace lpr {
 
 // plan-time spectra on the GPU (lpr_spectrum.cu)
 void spectrum_gpu(int device, const lpr_geometry& g, int kind, double* out);
+void rho_pad_multipliers(int device, int rows, int n, int nb, const double* mult, float2* d_out);
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
 __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const float* sino, float* qg);
@@ -122,6 +123,8 @@ struct lpr_gpu_plan {
     float2* mult_R = nullptr;
     float2* mult_B = nullptr;
     float2* mult_RT = nullptr;   // conj(mult_R): the transposed rho multiplier
+    int rho_pad = 0;             // padded rho-convolution length (non-smooth N_rho), 0: none
+    float2 *pad_R = nullptr, *pad_B = nullptr, *pad_RT = nullptr;  // its multipliers, (nts + 1) x rho_pad
     float* band = nullptr;       // banded transpose of the apron-extended 1-D prefilter
     int band_h = 0;
     float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
@@ -351,6 +354,35 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     p->mult_B = p->upload(mb);
     for (auto& v : mr) v.y = -v.y;
     p->mult_RT = p->upload(mr);
+    // non-7-smooth N_rho with a compile-time padded plan: the rho pass runs as a
+    // zero-padded linear convolution (k_rho_pad) with these padded multipliers
+    const char* pe = std::getenv("LPR_RHO_PAD");
+    p->rho_pad = (p->l_rho.variant == kFftGeneric && !(pe && pe[0] == '0')) ? int(rho_pad_length(int(nr))) : 0;
+    if (p->rho_pad) {
+        const long rr = nts + 1, nb = p->rho_pad;
+        std::vector<double> m64(2 * rr * nr);
+        auto build = [&](int which) {  // 0: R, 1: R#, 2: R^T (conjugate of R's)
+            for (long k = 0; k <= nts; ++k)
+                for (long v = 0; v < nr; ++v) {
+                    const long i = k * nr + v;
+                    cd z(0.0, 0.0);
+                    if (k < nts) {
+                        if (which == 1) z = cd(zeta_bp[2 * i], zeta_bp[2 * i + 1]) * (sb / (bhat(k, rows) * bhat(v, nr)));
+                        else z = cd(zeta[2 * i], zeta[2 * i + 1]) * (sr / bhat(v, nr));
+                        if (which == 2) z = std::conj(z);
+                    }
+                    m64[2 * i] = z.real();
+                    m64[2 * i + 1] = z.imag();
+                }
+        };
+        float2** dst[3] = {&p->pad_R, &p->pad_B, &p->pad_RT};
+        for (int w = 0; w < 3; ++w) {
+            build(w);
+            *dst[w] = p->dalloc<float2>(size_t(rr) * nb);
+            rho_pad_multipliers(p->device, int(rr), int(nr), int(nb), m64.data(), *dst[w]);
+        }
+        ck(prepare_rho_pad(), "rho pad smem attribute");
+    }
 
     // FBP transfer functions: DFT of the band-limited discrete
     // ramp kernel h(0) = 1/(4 ds^2), h(odd n) = -1/(n pi ds)^2 times ds, windowed
@@ -504,6 +536,16 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
 
 }
 
+// The rho convolution of every (k_theta, item) row: which = 0 (R), 1 (R#), 2 (R^T).
+void rho_chunk(lpr_gpu_plan* p, int which, int nb, cudaStream_t st, const DevGeom& g, float2* spec) {
+    const dim3 grid(g.nts + 1, nb * g.M);
+    if (p->rho_pad) {
+        launch_rho_pad(grid, st, g, which == 0 ? p->pad_R : which == 1 ? p->pad_B : p->pad_RT, spec);
+        return;
+    }
+    launch_rho_pass(p->l_rho, grid, st, g, p->d_rho, which == 0 ? p->mult_R : which == 1 ? p->mult_B : p->mult_RT, spec);
+}
+
 // Optional per-stage profiling: when p->prof is set, an event is recorded
 // before the first and after every launch (lpr_gpu_profile_stages).
 inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
@@ -548,7 +590,7 @@ void radon_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* img, float* s
     launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, S.q4, S.q4t, S.spec,
                            p->tex_mode);
     mark(p, 2, st);
-    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_R, S.spec);
+    rho_chunk(p, 0, nb, st, g, S.spec);
     mark(p, 3, st);
     launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.spec, S.lp);
     mark(p, 4, st);
@@ -571,7 +613,7 @@ void backproject_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* sino, f
     mark(p, 1, st);
     launch_bp_theta_fwd(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.qg, S.spec);
     mark(p, 2, st);
-    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_B, S.spec);
+    rho_chunk(p, 1, nb, st, g, S.spec);
     mark(p, 3, st);
     launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.spec, S.lp);
     mark(p, 4, st);
@@ -588,7 +630,7 @@ void transpose_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cud
     const DevGeom& g = p->g;
     k_radon_out_T<<<dim3(g.n_theta, nb), 256, g.n_rho * sizeof(float), st>>>(g, sino, p->lp);
     launch_theta_fwd_T(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->lp, p->spec);
-    launch_rho_pass(p->l_rho, dim3(g.nts + 1, nb * g.M), st, g, p->d_rho, p->mult_RT, p->spec);
+    rho_chunk(p, 2, nb, st, g, p->spec);
     ck(cudaMemsetAsync(p->qf, 0, sizeof(float) * size_t(nb) * g.pitch * g.pitch, st), "memset");
     launch_theta_inv_fine_T(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->spec, p->qf);
     k_prefilter_cols_T<<<dim3(cdiv(g.pitch, 256), g.N, nb), 256, 0, st>>>(g, p->band, p->band_h, p->qf, p->tmp);

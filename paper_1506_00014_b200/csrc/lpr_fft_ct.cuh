@@ -354,7 +354,7 @@ __device__ __forceinline__ void ct_mid_fused(float2* x, const TW* __restrict__ t
 // The buffer is free for the next TMA load once this returns.
 template <int N, int T, int S, int R, int OFF, class TW>
 __device__ __forceinline__ void ct_last_to_global(const float2* x, const TW* __restrict__ twp,
-                                                  float2* __restrict__ out, int tid) {
+                                                  float2* __restrict__ out, int tid, int n_out = N) {
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
     float2 v[NB][R];
@@ -380,7 +380,8 @@ __device__ __forceinline__ void ct_last_to_global(const float2* x, const TW* __r
             }
             Dft<R, true>::run(v[i]);
 #pragma unroll
-            for (int r = 0; r < R; ++r) out[b + r * B] = v[i][Dft<R, true>::slot(r)];
+            for (int r = 0; r < R; ++r)
+                if (N == n_out || b + r * B < n_out) out[b + r * B] = v[i][Dft<R, true>::slot(r)];
         }
     }
 }
@@ -426,7 +427,7 @@ struct RhoStream4 {
     static constexpr int kT = T;
     static constexpr int kElems = (ct_pad<S>(N - 1) + 2) / 2 * 2;
     __device__ __forceinline__ static void convolve(float2* x, const float4* twf4, const float4* twi4, const float2* ms,
-                                                    float2* out, int tid) {
+                                                    float2* out, int tid, int n_out = N) {
 #if LPR_RHO_TW_TABLE
         const float4 *twf = twf4, *twi = twi4;
 #else
@@ -438,7 +439,7 @@ struct RhoStream4 {
         ct_mid_fused<N, T, S, R4, R1 * (R2 - 1) + R1 * R2 * (R3 - 1)>(x, twf, ms, tid);
         ct_pass<N, T, S, R3, R4, 0, true>(x, twi, tid);
         ct_pass<N, T, S, R2, R4 * R3, R4 * (R3 - 1), true>(x, twi, tid);
-        ct_last_to_global<N, T, S, R1, R4 * (R3 - 1) + R4 * R3 * (R2 - 1)>(x, twi, out, tid);
+        ct_last_to_global<N, T, S, R1, R4 * (R3 - 1) + R4 * R3 * (R2 - 1)>(x, twi, out, tid, n_out);
     }
     static std::vector<float4> fwd_twiddles() {
         std::vector<float2> t;
@@ -486,6 +487,9 @@ using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16,
 using Fft8192Band = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 // streamed rho pass for N_rho = 4374 (2 rows in flight per block, 2 blocks per SM)
+// default-plan rho pass (N_rho = 4333 = 7 * 619): the circular convolution as
+// a zero-padded linear one over 8748 = 2^2 3^7 >= 2 N_rho - 1 (k_rho_pad)
+using RhoPad8748 = RhoStream4<8748, 512, 0, 9, 9, 9, 12>;
 // (radix 27,27,6 at 192 threads: 1.44 ms / 16 slices; 9,9,9,6 at 512 threads: 1.49)
 #ifndef LPR_RHO_RADIX9
 using Rho4374 = RhoStream<4374, 192, 0, 27, 27, 6>;

@@ -680,6 +680,35 @@ __global__ void __launch_bounds__(F::kT, 2) k_rho_stream(const __grid_constant__
     }
 }
 
+// Default-plan rho pass (N_rho not 7-smooth, e.g. 4333 = 7 * 619): the
+// circular convolution y = IDFT_n(M DFT_n(x)) equals the first n outputs of a
+// linear convolution with the n-periodised kernel, done as one zero-padded
+// transform pair of the 7-smooth length F::kN >= 2n - 1 with the padded
+// multiplier DFT_nb(periodised IDFT_n(M)) / nb (built once per plan on the
+// GPU in fp64, rho_pad_multipliers). One row per block, the multiplier read
+// from L2 inside the fused middle butterfly; replaces Bluestein (15x slower).
+template <class F>
+__global__ void __launch_bounds__(F::kT, 2) k_rho_pad(const __grid_constant__ DevGeom g,
+                                                      const float2* __restrict__ mult_pad, float2* __restrict__ spec) {
+    extern __shared__ __align__(16) float2 sm[];
+    const int k = blockIdx.x, item = blockIdx.y, n = g.n_rho, tid = threadIdx.x;
+    float2* row = spec + (size_t(item) * (g.nts + 1) + k) * n;
+    for (int j = tid; j < F::kN; j += F::kT) sm[j] = j < n ? row[j] : make_float2(0.f, 0.f);
+    __syncthreads();
+    F::convolve(sm, nullptr, nullptr, mult_pad + size_t(k) * F::kN, row, tid, n);
+}
+
+size_t rho_pad_length(int n_rho) { return (2 * n_rho - 1 <= RhoPad8748::kN && n_rho > 4096) ? RhoPad8748::kN : 0; }
+
+void launch_rho_pad(dim3 grid, cudaStream_t st, const DevGeom& g, const float2* mult_pad, float2* spec) {
+    k_rho_pad<RhoPad8748><<<grid, RhoPad8748::kT, sizeof(float2) * RhoPad8748::kElems, st>>>(g, mult_pad, spec);
+}
+
+cudaError_t prepare_rho_pad() {
+    return cudaFuncSetAttribute((const void*)k_rho_pad<RhoPad8748>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(float2) * RhoPad8748::kElems));
+}
+
 // Hermitian theta inverse: two real columns per complex transform of length
 // 2 nts; rows [j0, j0 + win) of the periodic result are kept.
 template <class F>

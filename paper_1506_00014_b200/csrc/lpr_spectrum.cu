@@ -161,6 +161,65 @@ void spectrum_device(const lpr_geometry& g, int kind, double* d_out, cudaStream_
     cudaFree(dcols);
 }
 
+__global__ void k_pad_periodise(const double2* __restrict__ m, double2* __restrict__ mt, int n, int nb) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+    if (t >= nb) return;
+    const double2* src = m + size_t(r) * n;
+    double2 v = make_double2(0.0, 0.0);
+    if (t < n) v = src[t];
+    else if (t > nb - n) v = src[t - nb + n];  // negative lags -(nb - t) of the n-periodic kernel
+    const double sc = 1.0 / double(nb);
+    mt[size_t(r) * nb + t] = make_double2(v.x * sc, v.y * sc);
+}
+
+__global__ void k_to_f32(const double2* __restrict__ a, float2* __restrict__ b, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        b[i] = make_float2(float(a[i].x), float(a[i].y));
+}
+
+// Padded multipliers of the default-plan rho pass (k_rho_pad): for every row
+// of the multiplier M (rows x n, fp64, host), DFT_nb of the n-periodised
+// kernel IDFT_n(M) over lags -(n-1)..n-1, divided by nb; fp32 into d_out
+// (rows x nb). Double-precision cuFFT (arbitrary n).
+void rho_pad_multipliers(int device, int rows, int n, int nb, const double* mult, float2* d_out) {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    double2 *dm = nullptr, *dt = nullptr;
+    const size_t bm = sizeof(double2) * size_t(rows) * n, bt = sizeof(double2) * size_t(rows) * nb;
+    ck(cudaMalloc(&dm, bm), "cudaMalloc");
+    if (cudaMalloc(&dt, bt) != cudaSuccess) {
+        cudaFree(dm);
+        throw CuErr("cudaMalloc: padded multipliers");
+    }
+    cufftHandle p1 = 0, p2 = 0;
+    try {
+        ck(cudaMemcpy(dm, mult, bm, cudaMemcpyHostToDevice), "H2D");
+        int ln = n, lb = nb;
+        ckf(cufftPlanMany(&p1, 1, &ln, nullptr, 1, ln, nullptr, 1, ln, CUFFT_Z2Z, rows), "cufftPlanMany");
+        ckf(cufftExecZ2Z(p1, reinterpret_cast<cufftDoubleComplex*>(dm), reinterpret_cast<cufftDoubleComplex*>(dm),
+                         CUFFT_INVERSE),
+            "cufftExecZ2Z");
+        k_pad_periodise<<<dim3((nb + 255) / 256, rows), 256>>>(dm, dt, n, nb);
+        ck(cudaGetLastError(), "periodise");
+        ckf(cufftPlanMany(&p2, 1, &lb, nullptr, 1, lb, nullptr, 1, lb, CUFFT_Z2Z, rows), "cufftPlanMany");
+        ckf(cufftExecZ2Z(p2, reinterpret_cast<cufftDoubleComplex*>(dt), reinterpret_cast<cufftDoubleComplex*>(dt),
+                         CUFFT_FORWARD),
+            "cufftExecZ2Z");
+        k_to_f32<<<1024, 256>>>(dt, d_out, size_t(rows) * nb);
+        ck(cudaGetLastError(), "to f32");
+        ck(cudaDeviceSynchronize(), "sync");
+    } catch (...) {
+        if (p1) cufftDestroy(p1);
+        if (p2) cufftDestroy(p2);
+        cudaFree(dm);
+        cudaFree(dt);
+        throw;
+    }
+    cufftDestroy(p1);
+    cufftDestroy(p2);
+    cudaFree(dm);
+    cudaFree(dt);
+}
+
 // Host-array form: computes on `device` and copies the (2 nts) x n_rho array back.
 void spectrum_gpu(int device, const lpr_geometry& g, int kind, double* out) {
     ck(cudaSetDevice(device), "cudaSetDevice");
