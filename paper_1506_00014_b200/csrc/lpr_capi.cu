@@ -220,7 +220,7 @@ struct lpr_gpu_plan {
         }
         if (launch.smem * launch.per_block > 227 * 1024 ||
             (staged_row && launch.smem + size_t(n) * sizeof(float2) > 227 * 1024))
-            throw std::invalid_argument("fft: transform does not fit in shared memory");
+            throw std::invalid_argument("fft: a length-" + std::to_string(n) + " transform does not fit in shared memory (for a non-7-smooth n_rho this large, use the 7-smooth plan: lpr_smooth_n_rho)");
     }
 
     ~lpr_gpu_plan() {
