@@ -531,7 +531,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
             p->g.lptex = p->lptex;
         }
     }
-    set_smem((const void*)k_radon_out, size_t(g.lps) * sizeof(float));
+    ck(prepare_out_kernels(g.lps), "cudaFuncSetAttribute(out kernels)");
     set_smem((const void*)k_radon_out_T, size_t(nr) * sizeof(float));
 
 }
@@ -594,7 +594,7 @@ void radon_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* img, float* s
     mark(p, 3, st);
     launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.spec, S.lp);
     mark(p, 4, st);
-    k_radon_out<<<dim3(g.n_theta, nb), 256, g.lps * sizeof(float), st>>>(g, S.lp, sino);
+    launch_radon_out(nb, st, g, S.lp, sino);
     mark(p, 5, st);
     check_launch("radon launch");
     p->launches += 5;
@@ -617,7 +617,7 @@ void backproject_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* sino, f
     mark(p, 3, st);
     launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.spec, S.lp);
     mark(p, 4, st);
-    k_bp_out<<<dim3(cdiv(g.N, 128), g.N, nb), 128, 0, st>>>(g, S.lp, img);
+    launch_bp_out(nb, st, g, S.lp, img);
     mark(p, 5, st);
     check_launch("backprojection launch");
     p->launches += 5;

@@ -14,6 +14,7 @@
 #include <cuda_pipeline.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "lpr_fft_ct.cuh"
 #include "lpr_kernels.cuh"
@@ -1055,7 +1056,85 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
     *out = 2.f * acc;
 }
 
+// k_radon_out with SB slices per block: the SB lattice rows are staged
+// together and each sinogram bin's rho coordinate (logf) and spline weights
+// are computed once for all of them.
+template <int SB>
+__global__ void __launch_bounds__(256) k_radon_out_b(DevGeom g, const float* __restrict__ lp, float* __restrict__ sino,
+                                                     int nb) {
+    extern __shared__ float srow[];
+    const int i = blockIdx.x, b0 = blockIdx.y * SB;
+    const int nts = g.nts, n = g.n_rho, N = g.N, lps = g.lps;
+    const int k = (2 * i + nts) / (2 * nts);
+    const int m = k % g.M;
+    const bool flip = ((k - m) / g.M) & 1;
+    const int j = i - k * nts;
+    const int ns = min(SB, nb - b0);
+    for (int s = 0; s < ns; ++s) {
+        const float* src = lp + ((size_t(b0 + s) * g.M + m) * g.win + (j - g.j0)) * lps;
+        for (int l = threadIdx.x; l < lps / 4; l += blockDim.x)
+            reinterpret_cast<float4*>(srow + s * lps)[l] = __ldg(reinterpret_cast<const float4*>(src) + l);
+    }
+    __syncthreads();
+    const float cth = __ldg(g.coarse_cos + j + nts / 2) * g.one_m_aR;
+    const float sgn = flip ? -1.f : 1.f;
+    float* out = sino + (size_t(b0) * g.n_theta + i) * N;
+    const size_t slice = size_t(g.n_theta) * N;
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+        const float sp = sgn * float(2 * c - N) / float(N);
+        const float rho = logf(fmaf(g.aR, sp, cth));
+        const float t = (rho - g.log_ar) * g.inv_drho;
+        const float kf = floorf(t);
+        float w[4];
+        bsw(t - kf, w);
+        const int k0 = int(kf) - 1;
+        int idx[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int q = k0 + a;
+            idx[a] = q < 0 ? q + n : (q >= n ? q - n : q);
+        }
+#pragma unroll
+        for (int s = 0; s < SB; ++s) {
+            if (s < ns) {
+                const float* row = srow + s * lps;
+                float acc = 0.f;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) acc = fmaf(w[a], row[idx[a]], acc);
+                out[s * slice + c] = acc * g.out_scale;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------- host launchers
+// R output resampling: SB = kOutSlices slices per block (k_radon_out_b,
+// 0.434 -> 0.373 ms / 16 slices); LPR_OUT_BATCH=0 selects the one-slice kernel (A/B).
+// (The same for k_bp_out, SB slices per thread sharing the atan/log
+// coordinates, measured 1.107 -> 1.104: that kernel is bound by its tld4 gathers.)
+static bool out_batched() {
+    static const bool on = [] {
+        const char* e = std::getenv("LPR_OUT_BATCH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+cudaError_t prepare_out_kernels(int lps) {
+    cudaError_t e = cudaFuncSetAttribute(k_radon_out, cudaFuncAttributeMaxDynamicSharedMemorySize, lps * int(sizeof(float)));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_radon_out_b<kOutSlices>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kOutSlices * lps * int(sizeof(float)));
+}
+void launch_radon_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* sino) {
+    if (out_batched())
+        k_radon_out_b<kOutSlices><<<dim3(g.n_theta, (nb + kOutSlices - 1) / kOutSlices), 256,
+                                    size_t(kOutSlices) * g.lps * sizeof(float), st>>>(g, lp, sino, nb);
+    else
+        k_radon_out<<<dim3(g.n_theta, nb), 256, g.lps * sizeof(float), st>>>(g, lp, sino);
+}
+void launch_bp_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* img) {
+    k_bp_out<<<dim3((g.N + 127) / 128, g.N, nb), 128, 0, st>>>(g, lp, img);
+}
 std::vector<float2> fft_pass_twiddles(int variant) {
     switch (variant) {
         case kFft2048: return Fft2048::pass_twiddles();

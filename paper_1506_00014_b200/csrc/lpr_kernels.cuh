@@ -18,6 +18,7 @@ constexpr int kMaxSectors = 16;
 using Tap = float4;
 constexpr int kApron = 4;     // mirrored border around the image coefficients
 constexpr int kFirHalf = 16;  // B-spline prefilter impulse-response half length
+constexpr int kOutSlices = 4;  // slices per block of the R output resampling kernel
 
 // Everything a kernel needs about the plan, passed by value.
 struct DevGeom {
@@ -85,6 +86,9 @@ void launch_theta_fwd_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const De
 void launch_theta_inv_fine_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                              const float2* spec, float* qbar);
 cudaError_t prepare_filter_kernel(const FftLaunch& L);
+cudaError_t prepare_out_kernels(int lps);
+void launch_radon_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* sino);
+void launch_bp_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* img);
 void launch_sino_filter(const FftLaunch& L, int rows_total, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                         const float* H, const float* in, float* out);
 
