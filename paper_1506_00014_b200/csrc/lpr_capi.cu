@@ -140,7 +140,8 @@ struct lpr_gpu_plan {
     cudaEvent_t ev_split[3] = {};
     int host_chunks = 16;                           // pipeline depth of the pinned host path (LPR_HOST_CHUNKS; 4/8/16 measured 684/798/813 e2e)
     bool split = false;                             // LPR_SPLIT=1: two staggered half batches (measured slower)
-    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    static constexpr int kHostSlots = 4;  // device staging slots of the pinned host pipeline
+    cudaEvent_t ev_h2d[kHostSlots] = {}, ev_comp[kHostSlots] = {}, ev_d2h[kHostSlots] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     bool tex_gather = false;      // LPR_PLAN_TEXTURE_GATHER ablation
     int tex_mode = 0;             // gather path of the R fine grid: 0 quad taps, 1 hardware bilinear (ablation)
@@ -229,7 +230,7 @@ struct lpr_gpu_plan {
         for (void* p : allocs) cudaFree(p);
         if (h_in) cudaFreeHost(h_in);
         if (h_out) cudaFreeHost(h_out);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kHostSlots; ++i) {
             if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
             if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
             if (ev_d2h[i]) cudaEventDestroy(ev_d2h[i]);
@@ -474,7 +475,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         const char* sp = std::getenv("LPR_SPLIT");
         p->split = sp && sp[0] == '1';
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < lpr_gpu_plan::kHostSlots; ++i) {
         ck(cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&p->ev_d2h[i], cudaEventDisableTiming), "cudaEventCreate");
@@ -759,16 +760,20 @@ void run_host(lpr_gpu_plan* p, ChunkFn fn, const float* hin, float* hout, int ba
         // ~8 chunks: the exposed pipeline fill (first H2D) and drain (last D2H) shrink with the chunk
         const int c = std::max(1, std::min(p->max_batch / 2, (batch + p->host_chunks - 1) / p->host_chunks));
         const int chunks = (batch + c - 1) / c;
+        // up to kHostSlots chunks in flight: a copy waits only for the compute
+        // (or D2H) of the chunk kHostSlots back, so jitter from other work on
+        // the device or the link (a concurrent call on another plan) is absorbed
+        const int slots = std::min(lpr_gpu_plan::kHostSlots, p->max_batch / c);
         for (int i = 0; i < chunks; ++i) {
-            const int slot = i & 1, b0 = i * c, nb = std::min(c, batch - b0);
+            const int slot = i % slots, b0 = i * c, nb = std::min(c, batch - b0);
             float* din = p->d_in + size_t(slot) * c * in_sz;
             float* dout = p->d_out + size_t(slot) * c * out_sz;
-            if (i >= 2) ck(cudaStreamWaitEvent(p->s_in, p->ev_comp[slot], 0), "wait");
+            if (i >= slots) ck(cudaStreamWaitEvent(p->s_in, p->ev_comp[slot], 0), "wait");
             ck(cudaMemcpyAsync(din, hin + size_t(b0) * in_sz, size_t(nb) * in_sz * sizeof(float),
                                cudaMemcpyHostToDevice, p->s_in), "H2D");
             ck(cudaEventRecord(p->ev_h2d[slot], p->s_in), "event");
             ck(cudaStreamWaitEvent(st, p->ev_h2d[slot], 0), "wait");
-            if (i >= 2) ck(cudaStreamWaitEvent(st, p->ev_d2h[slot], 0), "wait");
+            if (i >= slots) ck(cudaStreamWaitEvent(st, p->ev_d2h[slot], 0), "wait");
             fn(p, din, dout, nb, st);
             ck(cudaEventRecord(p->ev_comp[slot], st), "event");
             ck(cudaStreamWaitEvent(p->s_out, p->ev_comp[slot], 0), "wait");

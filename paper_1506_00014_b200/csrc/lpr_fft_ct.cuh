@@ -163,9 +163,20 @@ __device__ __forceinline__ void tw_apply_sincos(float2* v, int k, int L) {
     for (int r = 1; r < R; ++r) v[r] = cmul(v[r], p[r]);
 }
 
+// Band pruning of the pass before a final radix-2 (NS R = N/2) whose caller
+// needs only the outputs k with k mod N/2 in [0, BAND) or (N/2 - BAND, N/2):
+// output r of a butterfly lands at k + r NS (mod N/2), k < NS, so only the
+// r with r NS < BAND or r NS + NS - 1 > N/2 - BAND are stored (the dead
+// outputs' butterfly arithmetic is then dropped by the compiler).
+template <int N, int R, int NS, int BAND>
+__host__ __device__ constexpr bool band_keep(int r) {
+    return BAND == 0 || r * NS < BAND || r * NS + NS - 1 > N / 2 - BAND;
+}
+
 // One in-place pass of radix R at Stockham stride NS over a padded buffer.
-template <int N, int T, int S, int R, int NS, int OFF, bool INV, class TW>
+template <int N, int T, int S, int R, int NS, int OFF, bool INV, int BAND = 0, class TW>
 __device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, int tid) {
+    static_assert(BAND == 0 || NS * R * 2 == N, "band pruning applies to the pass before a final radix 2");
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
     float2 v[NB][R];
@@ -193,7 +204,8 @@ __device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, i
             Dft<R, INV>::run(v[i]);
             const int base = (b - k) * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[ct_pad<S>(base + r * NS)] = v[i][Dft<R, INV>::slot(r)];
+            for (int r = 0; r < R; ++r)
+                if (band_keep<N, R, NS, BAND>(r)) x[ct_pad<S>(base + r * NS)] = v[i][Dft<R, INV>::slot(r)];
         }
     }
     __syncthreads();
@@ -204,6 +216,15 @@ __device__ __forceinline__ void ct_run(float2* x, const TW* twp, int tid) {
     ct_pass<N, T, S, R, NS, OFF, INV>(x, twp, tid);
     if constexpr (sizeof...(Rest) > 0)
         ct_run<N, T, S, INV, NS * R, OFF + (NS > 1 ? NS * tw_rs(R) : 0), Rest...>(x, twp, tid);
+}
+template <int N, int T, int S, bool INV, int BAND, int NS, int OFF, int R, int... Rest, class TW>
+__device__ __forceinline__ void ct_run_band(float2* x, const TW* twp, int tid) {
+    if constexpr (sizeof...(Rest) > 0) {
+        ct_pass<N, T, S, R, NS, OFF, INV>(x, twp, tid);
+        ct_run_band<N, T, S, INV, BAND, NS * R, OFF + (NS > 1 ? NS * tw_rs(R) : 0), Rest...>(x, twp, tid);
+    } else {
+        ct_pass<N, T, S, R, NS, OFF, INV, BAND>(x, twp, tid);
+    }
 }
 
 // Host side: the per-pass table in exactly the order ct_run consumes it.
@@ -254,6 +275,10 @@ struct RadixPack {
     __device__ __forceinline__ static void tail(float2* x, const TW* twp, int tid) {
         if constexpr (sizeof...(Rest) > 0) ct_run<N, T, S, INV, R1, 0, Rest...>(x, twp, tid);
     }
+    template <int N, int T, int S, bool INV, int BAND, class TW>
+    __device__ __forceinline__ static void tail_band(float2* x, const TW* twp, int tid) {
+        if constexpr (sizeof...(Rest) > 0) ct_run_band<N, T, S, INV, BAND, R1, 0, Rest...>(x, twp, tid);
+    }
 };
 
 // FFT policies: idx() (the buffer slot of element i), elems() (shared
@@ -287,6 +312,11 @@ struct CtFft {
     template <bool INV>
     __device__ __forceinline__ static void run_tail(float2* x, const FftDesc& d, int gtid) {
         RadixPack<R...>::template tail<N, T, S, INV>(x, ct_tw(d), gtid);
+    }
+    // same, storing only what a band-limited final radix-2 reads (band_keep)
+    template <bool INV, int BAND>
+    __device__ __forceinline__ static void run_tail_band(float2* x, const FftDesc& d, int gtid) {
+        RadixPack<R...>::template tail_band<N, T, S, INV, BAND>(x, ct_tw(d), gtid);
     }
     static std::vector<float2> pass_twiddles() {
         std::vector<float2> t;

@@ -494,7 +494,9 @@ __device__ __forceinline__ float gather_tex(const DevGeom& g, const FineRow& r, 
 // zero-embed into the doubled fine period Lf, real theta FFT, keep |k| < nts.
 // Each thread gathers two fine rows per iteration (64 independent tap loads
 // in flight) to hide the L2 latency of the spline taps.
-template <class F, int TEX = 0, int PITCH = 0>
+// BAND = N/8 (the plan's |k| < nts band when refine = 4) prunes the
+// pass before the fused radix-2 store to the outputs that store reads.
+template <class F, int TEX = 0, int PITCH = 0, int BAND = 0>
 __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                             const Tap* __restrict__ qf, const Tap* __restrict__ qft,
                                             float2* __restrict__ spec) {
@@ -537,7 +539,10 @@ __global__ void LPR_LB(F) k_radon_theta_fwd(const __grid_constant__ DevGeom g, c
                     return make_float2(one ? gather_image<PITCH, !kScaleAtStore>(g, q, fr, vc, vr, er0, tq) : 0.f,
                                        two ? gather_image<PITCH, !kScaleAtStore>(g, q, fr, vc, vr, er1, tq) : 0.f);
             });
-            F::template run_tail<false>(sm, fd, G.tid);
+            if constexpr (BAND > 0)
+                F::template run_tail_band<false, BAND>(sm, fd, G.tid);
+            else
+                F::template run_tail<false>(sm, fd, G.tid);
             float2* out = spec + (size_t(b) * g.M + m) * size_t(g.nts + 1) * g.n_rho;
             if constexpr (F::kLast2)
                 store_half_spectra_r2<F>(Slots{smem, E}, Lf, g.nts, g.n_rho, l0b, out,
@@ -1204,6 +1209,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
     if (fine.variant == kFft8192) {
         SET(k_radon_theta_fwd<Fft8192Band>, fine.smem * fine.per_block);
         SET((k_radon_theta_fwd<Fft8192Band, 0, kPitch2048>), fine.smem * fine.per_block);
+        SET((k_radon_theta_fwd<Fft8192Band, 0, kPitch2048, 1024>), fine.smem * fine.per_block);
     }
 #define FINE(F)                                                   \
     SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block);         \
@@ -1235,7 +1241,14 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
     }
 #define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
     if (L.variant == kFft8192) {
-        if (g.pitch == kPitch2048)
+        static const bool band = [] {
+            const char* e = std::getenv("LPR_FINE_BAND");
+            return !(e && e[0] == '0');
+        }();
+        if (g.pitch == kPitch2048 && band && g.Lf == 8 * g.nts && g.nts == 1024)
+            k_radon_theta_fwd<Fft8192Band, 0, kPitch2048, 1024><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(
+                g, fd, qf, qft, spec);
+        else if (g.pitch == kPitch2048)
             k_radon_theta_fwd<Fft8192Band, 0, kPitch2048><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(
                 g, fd, qf, qft, spec);
         else

@@ -97,6 +97,31 @@ def test_host_entry_points_match_device(lp, lpo, cuda):
     np.testing.assert_array_equal(pipedb.numpy(), lp.fast_backprojection(piped.to(cuda), plan4).cpu().numpy())
 
 
+def test_two_plans_on_two_host_threads(lp, lpo, cuda):
+    """The bench's pipelined e2e leg: R on plan 1 and R# on plan 2 from two
+    host threads at once (pinned buffers, chunked pipelines on both) give the
+    same bits as the calls one after the other."""
+    import threading
+
+    import torch
+
+    N = 256
+    g, p, z, zb, plan1 = _setup(lp, lpo, N, max_batch=4)
+    plan2 = lp.RadonPlan(g, z, zb, max_batch=4)
+    f = torch.tensor(_inputs(lpo, N, 6).astype(np.float32)).pin_memory()
+    s_ref = lp.fast_radon(f, plan1)
+    b_ref = lp.fast_backprojection(s_ref, plan1)
+    out = {}
+    for _ in range(3):
+        t = threading.Thread(target=lambda: out.__setitem__("b", lp.fast_backprojection(s_ref, plan2)))
+        t.start()
+        out["s"] = lp.fast_radon(f, plan1)
+        t.join()
+        np.testing.assert_array_equal(out["s"].numpy(), s_ref.numpy())
+        np.testing.assert_array_equal(out["b"].numpy(), b_ref.numpy())
+    plan2.close()
+
+
 def test_zero_linearity_and_edge_cases(lp, lpo, cuda):
     import torch
 
