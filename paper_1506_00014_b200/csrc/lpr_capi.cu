@@ -124,6 +124,7 @@ struct lpr_gpu_plan {
     float2* mult_B = nullptr;
     float2* mult_RT = nullptr;   // conj(mult_R): the transposed rho multiplier
     int rho_pad = 0;             // padded rho-convolution length (non-smooth N_rho), 0: none
+    bool rho_direct = false;     // N_rho == that compile-time length: same kernel, plain multipliers
     float2 *pad_R = nullptr, *pad_B = nullptr, *pad_RT = nullptr;  // its multipliers, (nts + 1) x rho_pad
     float* band = nullptr;       // banded transpose of the apron-extended 1-D prefilter
     int band_h = 0;
@@ -359,6 +360,11 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     // zero-padded linear convolution (k_rho_pad) with these padded multipliers
     const char* pe = std::getenv("LPR_RHO_PAD");
     p->rho_pad = (p->l_rho.variant == kFftGeneric && !(pe && pe[0] == '0')) ? int(rho_pad_length(int(nr))) : 0;
+    // N_rho equal to the padded plan's length (8748: the N = 4096 bench plan):
+    // the same compile-time kernel runs the circular convolution directly with
+    // the plain multipliers (no padding)
+    p->rho_direct = p->l_rho.variant == kFftGeneric && !(pe && pe[0] == '0') && rho_direct_length() == size_t(nr);
+    if (p->rho_direct) ck(prepare_rho_pad(), "rho pad smem attribute");
     if (p->rho_pad) {
         const long rr = nts + 1, nb = p->rho_pad;
         std::vector<double> m64(2 * rr * nr);
@@ -542,6 +548,10 @@ void rho_chunk(lpr_gpu_plan* p, int which, int nb, cudaStream_t st, const DevGeo
     const dim3 grid(g.nts + 1, nb * g.M);
     if (p->rho_pad) {
         launch_rho_pad(grid, st, g, which == 0 ? p->pad_R : which == 1 ? p->pad_B : p->pad_RT, spec);
+        return;
+    }
+    if (p->rho_direct) {
+        launch_rho_pad(grid, st, g, which == 0 ? p->mult_R : which == 1 ? p->mult_B : p->mult_RT, spec);
         return;
     }
     launch_rho_pass(p->l_rho, grid, st, g, p->d_rho, which == 0 ? p->mult_R : which == 1 ? p->mult_B : p->mult_RT, spec);

@@ -32,6 +32,8 @@ __constant__ float4 c_wq12[12] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000
 __constant__ float4 c_wqc12[12] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {8.660254038e-01f, 5.000000000e-01f, -5.000000000e-01f, 8.660254038e-01f}, {5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, 5.000000000e-01f}, {6.123233996e-17f, 1.000000000e+00f, -1.000000000e+00f, 6.123233996e-17f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-8.660254038e-01f, 5.000000000e-01f, -5.000000000e-01f, -8.660254038e-01f}, {-1.000000000e+00f, 1.224646799e-16f, -1.224646799e-16f, -1.000000000e+00f}, {-8.660254038e-01f, -5.000000000e-01f, 5.000000000e-01f, -8.660254038e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-1.836970199e-16f, -1.000000000e+00f, 1.000000000e+00f, -1.836970199e-16f}, {5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, 5.000000000e-01f}, {8.660254038e-01f, -5.000000000e-01f, 5.000000000e-01f, 8.660254038e-01f}};
 __constant__ float4 c_wq16[16] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, 9.238795325e-01f}, {7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, 7.071067812e-01f}, {3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, 3.826834324e-01f}, {6.123233996e-17f, -1.000000000e+00f, 1.000000000e+00f, 6.123233996e-17f}, {-3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, -3.826834324e-01f}, {-7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f}, {-9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, -9.238795325e-01f}, {-1.000000000e+00f, -1.224646799e-16f, 1.224646799e-16f, -1.000000000e+00f}, {-9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, -9.238795325e-01f}, {-7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, -7.071067812e-01f}, {-3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, -3.826834324e-01f}, {-1.836970199e-16f, 1.000000000e+00f, -1.000000000e+00f, -1.836970199e-16f}, {3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, 3.826834324e-01f}, {7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f}, {9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, 9.238795325e-01f}};
 __constant__ float4 c_wqc16[16] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, 9.238795325e-01f}, {7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f}, {3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, 3.826834324e-01f}, {6.123233996e-17f, 1.000000000e+00f, -1.000000000e+00f, 6.123233996e-17f}, {-3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, -3.826834324e-01f}, {-7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, -7.071067812e-01f}, {-9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, -9.238795325e-01f}, {-1.000000000e+00f, 1.224646799e-16f, -1.224646799e-16f, -1.000000000e+00f}, {-9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, -9.238795325e-01f}, {-7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f}, {-3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, -3.826834324e-01f}, {-1.836970199e-16f, -1.000000000e+00f, 1.000000000e+00f, -1.836970199e-16f}, {3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, 3.826834324e-01f}, {7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, 7.071067812e-01f}, {9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, 9.238795325e-01f}};
+__constant__ float4 c_wq18[18] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, 9.396926208e-01f}, {7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, 7.660444431e-01f}, {5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, 5.000000000e-01f}, {1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, 1.736481777e-01f}, {-1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, -1.736481777e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, -7.660444431e-01f}, {-9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, -9.396926208e-01f}, {-1.000000000e+00f, -1.224646799e-16f, 1.224646799e-16f, -1.000000000e+00f}, {-9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, -9.396926208e-01f}, {-7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, -7.660444431e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, -1.736481777e-01f}, {1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, 1.736481777e-01f}, {5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, 5.000000000e-01f}, {7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, 7.660444431e-01f}, {9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, 9.396926208e-01f}};
+__constant__ float4 c_wqc18[18] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, 9.396926208e-01f}, {7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, 7.660444431e-01f}, {5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, 5.000000000e-01f}, {1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, 1.736481777e-01f}, {-1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, -1.736481777e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, -7.660444431e-01f}, {-9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, -9.396926208e-01f}, {-1.000000000e+00f, 1.224646799e-16f, -1.224646799e-16f, -1.000000000e+00f}, {-9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, -9.396926208e-01f}, {-7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, -7.660444431e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, -1.736481777e-01f}, {1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, 1.736481777e-01f}, {5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, 5.000000000e-01f}, {7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, 7.660444431e-01f}, {9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, 9.396926208e-01f}};
 __constant__ float4 c_wq27[27] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {9.730448706e-01f, -2.306158707e-01f, 2.306158707e-01f, 9.730448706e-01f}, {8.936326403e-01f, -4.487991802e-01f, 4.487991802e-01f, 8.936326403e-01f}, {7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, 7.660444431e-01f}, {5.971585917e-01f, -8.021231928e-01f, 8.021231928e-01f, 5.971585917e-01f}, {3.960797660e-01f, -9.182161069e-01f, 9.182161069e-01f, 3.960797660e-01f}, {1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, 1.736481777e-01f}, {-5.814482891e-02f, -9.983081583e-01f, 9.983081583e-01f, -5.814482891e-02f}, {-2.868032327e-01f, -9.579895123e-01f, 9.579895123e-01f, -2.868032327e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-6.862416379e-01f, -7.273736416e-01f, 7.273736416e-01f, -6.862416379e-01f}, {-8.354878114e-01f, -5.495089781e-01f, 5.495089781e-01f, -8.354878114e-01f}, {-9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, -9.396926208e-01f}, {-9.932383577e-01f, -1.160929141e-01f, 1.160929141e-01f, -9.932383577e-01f}, {-9.932383577e-01f, 1.160929141e-01f, -1.160929141e-01f, -9.932383577e-01f}, {-9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, -9.396926208e-01f}, {-8.354878114e-01f, 5.495089781e-01f, -5.495089781e-01f, -8.354878114e-01f}, {-6.862416379e-01f, 7.273736416e-01f, -7.273736416e-01f, -6.862416379e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-2.868032327e-01f, 9.579895123e-01f, -9.579895123e-01f, -2.868032327e-01f}, {-5.814482891e-02f, 9.983081583e-01f, -9.983081583e-01f, -5.814482891e-02f}, {1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, 1.736481777e-01f}, {3.960797660e-01f, 9.182161069e-01f, -9.182161069e-01f, 3.960797660e-01f}, {5.971585917e-01f, 8.021231928e-01f, -8.021231928e-01f, 5.971585917e-01f}, {7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, 7.660444431e-01f}, {8.936326403e-01f, 4.487991802e-01f, -4.487991802e-01f, 8.936326403e-01f}, {9.730448706e-01f, 2.306158707e-01f, -2.306158707e-01f, 9.730448706e-01f}};
 __constant__ float4 c_wqc27[27] = {{1.000000000e+00f, 0.000000000e+00f, -0.000000000e+00f, 1.000000000e+00f}, {9.730448706e-01f, 2.306158707e-01f, -2.306158707e-01f, 9.730448706e-01f}, {8.936326403e-01f, 4.487991802e-01f, -4.487991802e-01f, 8.936326403e-01f}, {7.660444431e-01f, 6.427876097e-01f, -6.427876097e-01f, 7.660444431e-01f}, {5.971585917e-01f, 8.021231928e-01f, -8.021231928e-01f, 5.971585917e-01f}, {3.960797660e-01f, 9.182161069e-01f, -9.182161069e-01f, 3.960797660e-01f}, {1.736481777e-01f, 9.848077530e-01f, -9.848077530e-01f, 1.736481777e-01f}, {-5.814482891e-02f, 9.983081583e-01f, -9.983081583e-01f, -5.814482891e-02f}, {-2.868032327e-01f, 9.579895123e-01f, -9.579895123e-01f, -2.868032327e-01f}, {-5.000000000e-01f, 8.660254038e-01f, -8.660254038e-01f, -5.000000000e-01f}, {-6.862416379e-01f, 7.273736416e-01f, -7.273736416e-01f, -6.862416379e-01f}, {-8.354878114e-01f, 5.495089781e-01f, -5.495089781e-01f, -8.354878114e-01f}, {-9.396926208e-01f, 3.420201433e-01f, -3.420201433e-01f, -9.396926208e-01f}, {-9.932383577e-01f, 1.160929141e-01f, -1.160929141e-01f, -9.932383577e-01f}, {-9.932383577e-01f, -1.160929141e-01f, 1.160929141e-01f, -9.932383577e-01f}, {-9.396926208e-01f, -3.420201433e-01f, 3.420201433e-01f, -9.396926208e-01f}, {-8.354878114e-01f, -5.495089781e-01f, 5.495089781e-01f, -8.354878114e-01f}, {-6.862416379e-01f, -7.273736416e-01f, 7.273736416e-01f, -6.862416379e-01f}, {-5.000000000e-01f, -8.660254038e-01f, 8.660254038e-01f, -5.000000000e-01f}, {-2.868032327e-01f, -9.579895123e-01f, 9.579895123e-01f, -2.868032327e-01f}, {-5.814482891e-02f, -9.983081583e-01f, 9.983081583e-01f, -5.814482891e-02f}, {1.736481777e-01f, -9.848077530e-01f, 9.848077530e-01f, 1.736481777e-01f}, {3.960797660e-01f, -9.182161069e-01f, 9.182161069e-01f, 3.960797660e-01f}, {5.971585917e-01f, -8.021231928e-01f, 8.021231928e-01f, 5.971585917e-01f}, {7.660444431e-01f, -6.427876097e-01f, 6.427876097e-01f, 7.660444431e-01f}, {8.936326403e-01f, -4.487991802e-01f, 4.487991802e-01f, 8.936326403e-01f}, {9.730448706e-01f, -2.306158707e-01f, 2.306158707e-01f, 9.730448706e-01f}};
 __constant__ float4 c_wq32[32] = {{1.000000000e+00f, -0.000000000e+00f, 0.000000000e+00f, 1.000000000e+00f}, {9.807852804e-01f, -1.950903220e-01f, 1.950903220e-01f, 9.807852804e-01f}, {9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, 9.238795325e-01f}, {8.314696123e-01f, -5.555702330e-01f, 5.555702330e-01f, 8.314696123e-01f}, {7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, 7.071067812e-01f}, {5.555702330e-01f, -8.314696123e-01f, 8.314696123e-01f, 5.555702330e-01f}, {3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, 3.826834324e-01f}, {1.950903220e-01f, -9.807852804e-01f, 9.807852804e-01f, 1.950903220e-01f}, {6.123233996e-17f, -1.000000000e+00f, 1.000000000e+00f, 6.123233996e-17f}, {-1.950903220e-01f, -9.807852804e-01f, 9.807852804e-01f, -1.950903220e-01f}, {-3.826834324e-01f, -9.238795325e-01f, 9.238795325e-01f, -3.826834324e-01f}, {-5.555702330e-01f, -8.314696123e-01f, 8.314696123e-01f, -5.555702330e-01f}, {-7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f}, {-8.314696123e-01f, -5.555702330e-01f, 5.555702330e-01f, -8.314696123e-01f}, {-9.238795325e-01f, -3.826834324e-01f, 3.826834324e-01f, -9.238795325e-01f}, {-9.807852804e-01f, -1.950903220e-01f, 1.950903220e-01f, -9.807852804e-01f}, {-1.000000000e+00f, -1.224646799e-16f, 1.224646799e-16f, -1.000000000e+00f}, {-9.807852804e-01f, 1.950903220e-01f, -1.950903220e-01f, -9.807852804e-01f}, {-9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, -9.238795325e-01f}, {-8.314696123e-01f, 5.555702330e-01f, -5.555702330e-01f, -8.314696123e-01f}, {-7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, -7.071067812e-01f}, {-5.555702330e-01f, 8.314696123e-01f, -8.314696123e-01f, -5.555702330e-01f}, {-3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, -3.826834324e-01f}, {-1.950903220e-01f, 9.807852804e-01f, -9.807852804e-01f, -1.950903220e-01f}, {-1.836970199e-16f, 1.000000000e+00f, -1.000000000e+00f, -1.836970199e-16f}, {1.950903220e-01f, 9.807852804e-01f, -9.807852804e-01f, 1.950903220e-01f}, {3.826834324e-01f, 9.238795325e-01f, -9.238795325e-01f, 3.826834324e-01f}, {5.555702330e-01f, 8.314696123e-01f, -8.314696123e-01f, 5.555702330e-01f}, {7.071067812e-01f, 7.071067812e-01f, -7.071067812e-01f, 7.071067812e-01f}, {8.314696123e-01f, 5.555702330e-01f, -5.555702330e-01f, 8.314696123e-01f}, {9.238795325e-01f, 3.826834324e-01f, -3.826834324e-01f, 9.238795325e-01f}, {9.807852804e-01f, 1.950903220e-01f, -1.950903220e-01f, 9.807852804e-01f}};
@@ -58,6 +60,7 @@ LPR_WQ(6)
 LPR_WQ(9)
 LPR_WQ(12)
 LPR_WQ(16)
+LPR_WQ(18)
 LPR_WQ(27)
 LPR_WQ(32)
 #undef LPR_WQ
@@ -112,6 +115,7 @@ LPR_DFT_PQ(6, 2, 3)
 LPR_DFT_PQ(9, 3, 3)
 LPR_DFT_PQ(12, 4, 3)
 LPR_DFT_PQ(16, 4, 4)
+LPR_DFT_PQ(18, 2, 9)
 LPR_DFT_PQ(27, 3, 9)
 LPR_DFT_PQ(32, 4, 8)
 #undef LPR_DFT_PQ
@@ -521,8 +525,13 @@ using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
 // a zero-padded linear one over 8748 = 2^2 3^7 >= 2 N_rho - 1 (k_rho_pad)
 using RhoPad8748 = RhoStream4<8748, 512, 0, 9, 9, 9, 12>;
 // (radix 27,27,6 at 192 threads: 1.44 ms / 16 slices; 9,9,9,6 at 512 threads: 1.49)
-#ifndef LPR_RHO_RADIX9
-using Rho4374 = RhoStream<4374, 192, 0, 27, 27, 6>;
+#ifndef LPR_RHO_T
+#define LPR_RHO_T 192
+#endif
+#if defined(LPR_RHO_R18)
+using Rho4374 = RhoStream<4374, LPR_RHO_T, 0, 9, 27, 18>;
+#elif !defined(LPR_RHO_RADIX9)
+using Rho4374 = RhoStream<4374, LPR_RHO_T, 0, 27, 27, 6>;
 #else
 using Rho4374 = RhoStream4<4374, 512, 0, 9, 9, 9, 6>;
 #endif

@@ -704,6 +704,8 @@ __global__ void __launch_bounds__(F::kT, 2) k_rho_pad(const __grid_constant__ De
     F::convolve(sm, nullptr, nullptr, mult_pad + size_t(k) * F::kN, row, tid, n);
 }
 
+size_t rho_direct_length() { return RhoPad8748::kN; }
+
 size_t rho_pad_length(int n_rho) { return (2 * n_rho - 1 <= RhoPad8748::kN && n_rho > 4096) ? RhoPad8748::kN : 0; }
 
 void launch_rho_pad(dim3 grid, cudaStream_t st, const DevGeom& g, const float2* mult_pad, float2* spec) {
