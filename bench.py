@@ -147,7 +147,8 @@ def measured_peak():
 STAGE_KERNELS = {
     "prefilter_2d": ("k_prefilter_2d_iir",),
     "prefilter_sino": ("k_prefilter_sino_iir",),
-    "rho_pass": ("k_rho_stream", "k_rho_pass"),
+    "rho_pass": ("k_rho_stream", "k_rho_pass", "k_rho_pad"),
+    "radon_out": ("k_radon_out_b", "k_radon_out"),
 }
 
 

@@ -520,6 +520,8 @@ using Fft8192 = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16,
 // the fine theta forward of R: same plan without the last radix-2 pass
 using Fft8192Band = CtFft<8192, 512, LPR_FFT8192_P, LPR_FFT8192_MINB, 4, 16, 16, 16>;
 using Fft16384 = CtFft<16384, 512, 1, 1, 5, 32, 32, 16>;
+// the fine theta forward of R at N = 4096: last radix 2 fused into the band store
+using Fft16384Band = CtFft<16384, 512, 1, 1, 5, 32, 32, 8>;
 // streamed rho pass for N_rho = 4374 (2 rows in flight per block, 2 blocks per SM)
 // default-plan rho pass (N_rho = 4333 = 7 * 619): the circular convolution as
 // a zero-padded linear one over 8748 = 2^2 3^7 >= 2 N_rho - 1 (k_rho_pad)

@@ -1213,6 +1213,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
         SET((k_radon_theta_fwd<Fft8192Band, 0, kPitch2048>), fine.smem * fine.per_block);
         SET((k_radon_theta_fwd<Fft8192Band, 0, kPitch2048, 1024>), fine.smem * fine.per_block);
     }
+    if (fine.variant == kFft16384) SET((k_radon_theta_fwd<Fft16384Band, 0, 0, 2048>), fine.smem * fine.per_block);
 #define FINE(F)                                                   \
     SET(k_radon_theta_fwd<F>, fine.smem * fine.per_block);         \
     SET((k_radon_theta_fwd<F, 1>), fine.smem * fine.per_block);    \
@@ -1242,11 +1243,11 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
         return;
     }
 #define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
+    static const bool band = [] {  // LPR_FINE_BAND=0: the unpruned plans (A/B)
+        const char* e = std::getenv("LPR_FINE_BAND");
+        return !(e && e[0] == '0');
+    }();
     if (L.variant == kFft8192) {
-        static const bool band = [] {
-            const char* e = std::getenv("LPR_FINE_BAND");
-            return !(e && e[0] == '0');
-        }();
         if (g.pitch == kPitch2048 && band && g.Lf == 8 * g.nts && g.nts == 1024)
             k_radon_theta_fwd<Fft8192Band, 0, kPitch2048, 1024><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(
                 g, fd, qf, qft, spec);
@@ -1255,6 +1256,11 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
                 g, fd, qf, qft, spec);
         else
             CALL(Fft8192Band);
+        return;
+    }
+    if (L.variant == kFft16384 && band && g.Lf == 8 * g.nts && g.nts == 2048) {  // N = 4096: band-pruned, radix 2 fused into the store
+        k_radon_theta_fwd<Fft16384Band, 0, 0, 2048><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(
+            g, fd, qf, qft, spec);
         return;
     }
     LPR_FFT_SWITCH(L.variant, CALL)
