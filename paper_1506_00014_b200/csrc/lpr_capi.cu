@@ -24,7 +24,6 @@ void spectrum_gpu(int device, const lpr_geometry& g, int kind, double* out);
 void rho_pad_multipliers(int device, int rows, int n, int nb, const double* mult, float2* d_out);
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
-__global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const float* sino, float* qg);
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
 __global__ void k_bp_out(DevGeom g, const float* lp, float* img);
 __global__ void k_radon_out_T(DevGeom g, const float* sino, float* lp);
@@ -539,6 +538,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         }
     }
     ck(prepare_out_kernels(g.lps), "cudaFuncSetAttribute(out kernels)");
+    ck(prepare_prefilter_sino(), "cudaFuncSetAttribute(prefilter_sino)");
     set_smem((const void*)k_radon_out_T, size_t(nr) * sizeof(float));
 
 }
@@ -619,7 +619,7 @@ const char* const kRadonStages[] = {"prefilter_2d", "radon_theta_fwd", "rho_pass
 void backproject_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* sino, float* img, int nb, cudaStream_t st) {
     const DevGeom& g = S.g;
     mark(p, 0, st);
-    k_prefilter_sino_iir<<<dim3(cdiv(g.N, 256), cdiv(g.n_theta, 32), nb), 128, 0, st>>>(g, sino, S.qg);
+    launch_prefilter_sino(nb, st, g, sino, S.qg);
     first_done(S, st);
     mark(p, 1, st);
     launch_bp_theta_fwd(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.qg, S.spec);

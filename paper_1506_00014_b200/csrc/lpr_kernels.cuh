@@ -88,6 +88,8 @@ void launch_theta_inv_fine_T(const FftLaunch& L, dim3 grid, cudaStream_t st, con
                              const float2* spec, float* qbar);
 cudaError_t prepare_filter_kernel(const FftLaunch& L);
 cudaError_t prepare_out_kernels(int lps);
+cudaError_t prepare_prefilter_sino();
+void launch_prefilter_sino(int nb, cudaStream_t st, const DevGeom& g, const float* sino, float* qg);
 void launch_radon_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* sino);
 void launch_bp_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* img);
 void launch_sino_filter(const FftLaunch& L, int rows_total, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
