@@ -25,7 +25,6 @@ void rho_pad_multipliers(int device, int rows, int n, int nb, const double* mult
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
 __global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
-__global__ void k_bp_out(DevGeom g, const float* lp, float* img);
 __global__ void k_radon_out_T(DevGeom g, const float* sino, float* lp);
 __global__ void k_prefilter_cols_T(DevGeom g, const float* band, int H, const float* qbar, float* tmp);
 __global__ void k_prefilter_rows_T(DevGeom g, const float* band, int H, const float* tmp, float* img, float scale);
