@@ -289,6 +289,30 @@ template <class F>
 __device__ __forceinline__ void store_half_spectra(Slots res, int L, int nts, int n_rho, int l0,
                                                    float2* __restrict__ out) {
     constexpr int P = F::kP;
+    if constexpr (F::kT > 0) {
+        // compile-time block size: one pair per thread, rows tid / P + j kT (index math hoisted)
+        const int p = threadIdx.x % P, l = l0 + 2 * p;
+        if (l >= n_rho) return;
+        const float2* x = res(p);
+        float2* dst0 = out + l;
+        const bool two = l + 1 < n_rho;
+        for (int k = threadIdx.x / P; k <= nts; k += F::kT) {
+            float2 A = make_float2(0.f, 0.f), B = A;
+            if (k < nts) {
+                const float2 z = x[F::idx(k)], zm = x[F::idx(k == 0 ? 0 : L - k)];
+                A = make_float2(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y));
+                B = make_float2(0.5f * (z.y + zm.y), -0.5f * (z.x - zm.x));
+            }
+            float2* dst = dst0 + size_t(k) * n_rho;
+            if (two && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                *reinterpret_cast<float4*>(dst) = make_float4(A.x, A.y, B.x, B.y);
+            } else {
+                dst[0] = A;
+                if (two) dst[1] = B;
+            }
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < (nts + 1) * P; e += blockDim.x) {
         const int k = e / P, p = e % P;
         const int l = l0 + 2 * p;
@@ -356,6 +380,39 @@ template <class F>
 __device__ __forceinline__ void load_packed_hermitian(Slots sm, const float2* __restrict__ in, int kmax,
                                                       int L, int n, int l0) {
     constexpr int P = F::kP;
+    if constexpr (F::kT > 0) {
+        // compile-time block size: a thread keeps one column pair p and walks
+        // rows k = tid / P + j RS, so the index math is hoisted out of the loop
+        // (the integer pipe was this kernel's busiest)
+        constexpr int BT = F::kT * P, RS = BT / P;
+        constexpr int U = 8;  // independent 16-byte loads in flight per thread
+        const int p = threadIdx.x % P, k0 = threadIdx.x / P;
+        const int l = l0 + 2 * p;
+        const bool vec = l + 2 <= n && (n % 2) == 0 && (reinterpret_cast<uintptr_t>(in + l) & 15) == 0;
+        float2* dst = sm(p);
+        if (vec && l0 + 2 * P <= n) {
+            const float4* src = reinterpret_cast<const float4*>(in + l);
+            const int n4 = n / 2;  // float4 row stride
+            for (int kb = k0; kb < kmax; kb += U * RS) {
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = kb + u * RS;
+                    if (k < kmax) v[u] = __ldg(src + size_t(k) * n4);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = kb + u * RS;
+                    if (k < kmax) {
+                        const float2 A = make_float2(v[u].x, v[u].y), B = make_float2(v[u].z, v[u].w);
+                        dst[F::idx(k)] = make_float2(A.x - B.y, A.y + B.x);
+                        if (k > 0) dst[F::idx(L - k)] = make_float2(A.x + B.y, B.x - A.y);
+                    }
+                }
+            }
+            return;
+        }
+    }
 #ifndef LPR_HERM_U
 #define LPR_HERM_U 8
 #endif
@@ -750,6 +807,34 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
     float2* res = F::template run<true>(sms(G.g), fft_scratch<F>(sms(G.g), fd), fd, G.tid);
     const Slots rs = result_slots<F>(smem, E, res);
     float* out = lp + item * size_t(g.win) * g.lps;
+    if constexpr (F::kT > 0) {
+        // one column pair per thread, rows tid / P + j RS; the window rows
+        // r < -j0 come from the top of the period (q + L2)
+        constexpr int RS = F::kT;  // = blockDim.x / P
+        const int p = threadIdx.x % P, l = l0b + 2 * p;
+        if (l < n) {
+            const float2* src = rs(p);
+            float* dst = out + l;
+            const bool pair = l + 1 < n && (reinterpret_cast<uintptr_t>(dst) & 7) == 0 && (g.lps % 2) == 0;
+            const int wrap = -g.j0;  // rows [0, wrap) read slot j0 + r + L2
+            for (int r = threadIdx.x / P; r < g.win; r += RS) {
+                const int q = g.j0 + r + (r < wrap ? L2 : 0);
+                const float2 z = src[F::idx(q)];
+                float* d = dst + size_t(r) * g.lps;
+                if (pair) {
+                    *reinterpret_cast<float2*>(d) = z;
+                } else {
+                    d[0] = z.x;
+                    if (l + 1 < n) d[1] = z.y;
+                }
+                if (l < 3) {  // periodic copy of columns 0..2 past the end: rho taps never wrap
+                    d[n] = z.x;
+                    if (l + 1 < 3) d[n + 1] = z.y;
+                }
+            }
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < g.win * P; e += blockDim.x) {
         const int r = e / P, p = e % P;
         const int l = l0b + 2 * p;
@@ -1004,6 +1089,10 @@ __global__ void LPR_LB(F) k_sino_filter(const __grid_constant__ DevGeom g, const
 }
 
 // T_m^{-1} Omega_p -> X resampling and the sector sum (Alg. 2 steps 5-7).
+// MC > 0: the sector count at compile time, so the sector loop unrolls and
+// every sector's texture gathers can be in flight together (the kernel waits
+// on tld4 latency: long-scoreboard stalls dominate its ncu profile).
+template <int MC>
 __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restrict__ img) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int r = blockIdx.y, b = blockIdx.z;
@@ -1017,7 +1106,9 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
     }
     const float xp = float(dxr) / float(N), yp = float(dyr) / float(N);
     float acc = 0.f;
-    for (int m = 0; m < g.M; ++m) {
+    const int M = MC > 0 ? MC : g.M;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
         const float cm = g.cosm[m], smm = g.sinm[m];
         const float yx = fmaf(g.aR, fmaf(cm, xp, smm * yp), g.one_m_aR);
         const float yy = g.aR * fmaf(-smm, xp, cm * yp);
@@ -1039,7 +1130,7 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         const float* base = lp + (size_t(b) * g.M + m) * size_t(g.win) * g.lps + (int(kt) - 1 - g.j0) * g.lps;
         const int c0 = int(kr) - 1;
         float sacc = 0.f;
-        if (g.lptex) {  // four tld4 gathers (2 x 2 texels each, exact fp32)
+        if (MC > 0 || g.lptex) {  // four tld4 gathers (2 x 2 texels each, exact fp32); MC > 0 only with the texture
             const float x0 = float(c0 + 1), x1 = x0 + 2.f;
             const float y0 = float(((b + g.sb0) * g.M + m) * g.win + int(kt) - 1 - g.j0) + 1.f, y1 = y0 + 2.f;
             const float4 a = tex2Dgather<float4>(g.lptex, x0, y0, 0), e = tex2Dgather<float4>(g.lptex, x1, y0, 0);
@@ -1153,7 +1244,15 @@ void launch_radon_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp
         k_radon_out<<<dim3(g.n_theta, nb), 256, g.lps * sizeof(float), st>>>(g, lp, sino);
 }
 void launch_bp_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* img) {
-    k_bp_out<<<dim3((g.N + 127) / 128, g.N, nb), 128, 0, st>>>(g, lp, img);
+    static const bool unroll = [] {  // LPR_BP_UNROLL=0: runtime sector loop (A/B)
+        const char* e = std::getenv("LPR_BP_UNROLL");
+        return !(e && e[0] == '0');
+    }();
+    const dim3 grid((g.N + 127) / 128, g.N, nb);
+    if (unroll && g.M == 3 && g.lptex)
+        k_bp_out<3><<<grid, 128, 0, st>>>(g, lp, img);
+    else
+        k_bp_out<0><<<grid, 128, 0, st>>>(g, lp, img);
 }
 std::vector<float2> fft_pass_twiddles(int variant) {
     switch (variant) {
