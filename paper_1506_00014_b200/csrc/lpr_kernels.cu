@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const flo
     __syncthreads();
     // transposed store (Qg^T[b][s][theta], see gather_sino): a warp writes 32
     // consecutive theta of one s column; the odd pitch keeps the reads conflict-free
-    for (int idx = tid; idx < kSRows * kSCols; idx += blockDim.x) {
+    for (int idx = tid; idx < kSRows * kSCols; idx += 128) {
         const int i = idx % kSRows, j = idx / kSRows;
         if (i < rows && c0col + j < N) qg[(size_t(b) * N + c0col + j) * g.n_theta + i0 + i] = s[i * kSP + kIW + j];
     }
@@ -343,7 +343,7 @@ __device__ __forceinline__ void store_half_spectra_r2(Slots res, int L, int nts,
     const float h0 = 0.5f * s0, h1 = 0.5f * s1;  // column scales (P = 1), with the 1/2 of the split
     constexpr int P = F::kP;
     const int H = L / 2;
-    for (int e = threadIdx.x; e < (nts + 1) * P; e += blockDim.x) {
+    for (int e = threadIdx.x; e < (nts + 1) * P; e += (F::kT > 0 ? F::kT * F::kP : int(blockDim.x))) {
         const int k = e / P, p = e % P;
         const int l = l0b + 2 * p;
         if (l >= n_rho) continue;
@@ -1089,10 +1089,6 @@ __global__ void LPR_LB(F) k_sino_filter(const __grid_constant__ DevGeom g, const
 }
 
 // T_m^{-1} Omega_p -> X resampling and the sector sum (Alg. 2 steps 5-7).
-// MC > 0: the sector count at compile time, so the sector loop unrolls and
-// every sector's texture gathers can be in flight together (the kernel waits
-// on tld4 latency: long-scoreboard stalls dominate its ncu profile).
-template <int MC>
 __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restrict__ img) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int r = blockIdx.y, b = blockIdx.z;
@@ -1106,9 +1102,7 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
     }
     const float xp = float(dxr) / float(N), yp = float(dyr) / float(N);
     float acc = 0.f;
-    const int M = MC > 0 ? MC : g.M;
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
+    for (int m = 0; m < g.M; ++m) {
         const float cm = g.cosm[m], smm = g.sinm[m];
         const float yx = fmaf(g.aR, fmaf(cm, xp, smm * yp), g.one_m_aR);
         const float yy = g.aR * fmaf(-smm, xp, cm * yp);
@@ -1130,7 +1124,7 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         const float* base = lp + (size_t(b) * g.M + m) * size_t(g.win) * g.lps + (int(kt) - 1 - g.j0) * g.lps;
         const int c0 = int(kr) - 1;
         float sacc = 0.f;
-        if (MC > 0 || g.lptex) {  // four tld4 gathers (2 x 2 texels each, exact fp32); MC > 0 only with the texture
+        if (g.lptex) {  // four tld4 gathers (2 x 2 texels each, exact fp32)
             const float x0 = float(c0 + 1), x1 = x0 + 2.f;
             const float y0 = float(((b + g.sb0) * g.M + m) * g.win + int(kt) - 1 - g.j0) + 1.f, y1 = y0 + 2.f;
             const float4 a = tex2Dgather<float4>(g.lptex, x0, y0, 0), e = tex2Dgather<float4>(g.lptex, x1, y0, 0);
@@ -1183,7 +1177,7 @@ __global__ void __launch_bounds__(256) k_radon_out_b(DevGeom g, const float* __r
     const int ns = min(SB, nb - b0);
     for (int s = 0; s < ns; ++s) {
         const float* src = lp + ((size_t(b0 + s) * g.M + m) * g.win + (j - g.j0)) * lps;
-        for (int l = threadIdx.x; l < lps / 4; l += blockDim.x)
+        for (int l = threadIdx.x; l < lps / 4; l += 256)
             reinterpret_cast<float4*>(srow + s * lps)[l] = __ldg(reinterpret_cast<const float4*>(src) + l);
     }
     __syncthreads();
@@ -1191,7 +1185,7 @@ __global__ void __launch_bounds__(256) k_radon_out_b(DevGeom g, const float* __r
     const float sgn = flip ? -1.f : 1.f;
     float* out = sino + (size_t(b0) * g.n_theta + i) * N;
     const size_t slice = size_t(g.n_theta) * N;
-    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    for (int c = threadIdx.x; c < N; c += 256) {
         const float sp = sgn * float(2 * c - N) / float(N);
         const float rho = logf(fmaf(g.aR, sp, cth));
         const float t = (rho - g.log_ar) * g.inv_drho;
@@ -1244,15 +1238,8 @@ void launch_radon_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp
         k_radon_out<<<dim3(g.n_theta, nb), 256, g.lps * sizeof(float), st>>>(g, lp, sino);
 }
 void launch_bp_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* img) {
-    static const bool unroll = [] {  // LPR_BP_UNROLL=0: runtime sector loop (A/B)
-        const char* e = std::getenv("LPR_BP_UNROLL");
-        return !(e && e[0] == '0');
-    }();
-    const dim3 grid((g.N + 127) / 128, g.N, nb);
-    if (unroll && g.M == 3 && g.lptex)
-        k_bp_out<3><<<grid, 128, 0, st>>>(g, lp, img);
-    else
-        k_bp_out<0><<<grid, 128, 0, st>>>(g, lp, img);
+    // (the sector loop unrolled for M = 3, all 12 tld4 gathers in flight: 1.107 -> 1.106)
+    k_bp_out<<<dim3((g.N + 127) / 128, g.N, nb), 128, 0, st>>>(g, lp, img);
 }
 std::vector<float2> fft_pass_twiddles(int variant) {
     switch (variant) {
