@@ -103,7 +103,7 @@ __device__ __forceinline__ void stage_rows(float* s, const float* __restrict__ s
 }
 
 template <class T>
-__global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float* __restrict__ img, T* __restrict__ q4,
+__global__ void __launch_bounds__(128, 5) k_prefilter_2d_iir(DevGeom g, const float* __restrict__ img, T* __restrict__ q4,
                                                           T* __restrict__ q4t) {
     __shared__ float s[kIR][kICP];
     constexpr float z = -0.26794919243112270647f;
@@ -144,25 +144,39 @@ __global__ void __launch_bounds__(128) k_prefilter_2d_iir(DevGeom g, const float
         for (int k = kIR - 2; k >= 0; --k) s[k][j] = d = z * (d - s[k][j]);
     }
     __syncthreads();
+    // stores (128 threads, launch_prefilter_2d): a thread keeps one tile column
+    // (row-major quads) or one tile row (transposed quads) and steps the other
+    // index by 2, so the index math is hoisted out of the loop
+    static_assert(kIT == 64, "the store loops assume 128 threads over 64-wide tiles");
     T* dst = q4 + size_t(b) * pitch * pitch;
-    for (int idx = tid; idx < kIT * kIT; idx += blockDim.x) {
-        const int i = idx / kIT, j = idx % kIT;
-        if (y0 + i >= pitch || x0 + j >= pitch) continue;
-        const float* r = s[kIW + i] + kIW + j;
-        if constexpr (sizeof(T) == sizeof(float4)) {
-            dst[size_t(y0 + i) * pitch + x0 + j] = make_float4(r[0], r[1], r[2], r[3]);
-        } else {
-            dst[size_t(y0 + i) * pitch + x0 + j] = r[0];
+    {
+        const int j = tid & (kIT - 1);
+        if (x0 + j < pitch) {
+            T* d = dst + size_t(y0) * pitch + x0 + j;
+#pragma unroll 2
+            for (int i = tid >> 6; i < kIT; i += 2) {
+                if (y0 + i >= pitch) break;
+                const float* r = s[kIW + i] + kIW + j;
+                if constexpr (sizeof(T) == sizeof(float4)) {
+                    d[size_t(i) * pitch] = make_float4(r[0], r[1], r[2], r[3]);
+                } else {
+                    d[size_t(i) * pitch] = r[0];
+                }
+            }
         }
     }
     if constexpr (sizeof(T) == sizeof(float4)) {
         if (q4t) {  // transposed quads qt[c][r] = Q[r..r+3][c] (read by sector 0); a warp writes 32 consecutive r
-            T* dt = q4t + size_t(b) * pitch * pitch;
-            for (int idx = tid; idx < kIT * kIT; idx += blockDim.x) {
-                const int i = idx % kIT, j = idx / kIT;
-                if (y0 + i >= pitch || x0 + j >= pitch) continue;
-                const float* r = s[kIW + i] + kIW + j;
-                dt[size_t(x0 + j) * pitch + y0 + i] = make_float4(r[0], r[kICP], r[2 * kICP], r[3 * kICP]);
+            const int i = tid & (kIT - 1);
+            if (y0 + i < pitch) {
+                T* dt = q4t + size_t(b) * pitch * pitch + size_t(x0) * pitch + y0 + i;
+                const float* r0 = s[kIW + i] + kIW;
+#pragma unroll 2
+                for (int j = tid >> 6; j < kIT; j += 2) {
+                    if (x0 + j >= pitch) break;
+                    const float* r = r0 + j;
+                    dt[size_t(j) * pitch] = make_float4(r[0], r[kICP], r[2 * kICP], r[3 * kICP]);
+                }
             }
         }
     }
@@ -904,6 +918,12 @@ __device__ __forceinline__ float gather_sino(const float* __restrict__ row, int 
     bsw(t - kf, w);
     const int k0 = int(kf) - 1;
     float acc = 0.f;
+    if (k0 >= 0 && k0 + 3 < N) {  // all four taps on the detector (the common case): no per-tap tests
+        const float* p = row + size_t(k0) * ld;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) acc = fmaf(w[a], __ldg(p + a * ld), acc);
+        return acc;
+    }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int idx = k0 + a;
