@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 300 python scripts/stage_times.py 2048 16 > gpurun_out/st_pf2.json 2>&1
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest.txt
+timeout 300 python scripts/stage_times.py 2048 16 > gpurun_out/st_invn.json 2>&1

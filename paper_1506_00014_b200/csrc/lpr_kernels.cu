@@ -888,9 +888,10 @@ __global__ void k_radon_out(DevGeom g, const float* __restrict__ lp, float* __re
     __syncthreads();
     const float cth = __ldg(g.coarse_cos + j + nts / 2) * g.one_m_aR;
     const float sgn = flip ? -1.f : 1.f;
+    const float invN = 1.f / float(N);
     float* out = sino + (size_t(b) * g.n_theta + i) * N;
     for (int c = threadIdx.x; c < N; c += blockDim.x) {
-        const float sp = sgn * float(2 * c - N) / float(N);
+        const float sp = sgn * float(2 * c - N) * invN;  // (x / N exactly for power-of-two N)
         const float rho = logf(fmaf(g.aR, sp, cth));
         const float t = (rho - g.log_ar) * g.inv_drho;
         const float kf = floorf(t);
@@ -1120,7 +1121,8 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         *out = 0.f;
         return;
     }
-    const float xp = float(dxr) / float(N), yp = float(dyr) / float(N);
+    const float invN = 1.f / float(N);
+    const float xp = float(dxr) * invN, yp = float(dyr) * invN;
     float acc = 0.f;
     for (int m = 0; m < g.M; ++m) {
         const float cm = g.cosm[m], smm = g.sinm[m];
@@ -1203,10 +1205,11 @@ __global__ void __launch_bounds__(256) k_radon_out_b(DevGeom g, const float* __r
     __syncthreads();
     const float cth = __ldg(g.coarse_cos + j + nts / 2) * g.one_m_aR;
     const float sgn = flip ? -1.f : 1.f;
+    const float invN = 1.f / float(N);
     float* out = sino + (size_t(b0) * g.n_theta + i) * N;
     const size_t slice = size_t(g.n_theta) * N;
     for (int c = threadIdx.x; c < N; c += 256) {
-        const float sp = sgn * float(2 * c - N) / float(N);
+        const float sp = sgn * float(2 * c - N) * invN;  // (x / N exactly for power-of-two N)
         const float rho = logf(fmaf(g.aR, sp, cth));
         const float t = (rho - g.log_ar) * g.inv_drho;
         const float kf = floorf(t);

@@ -42,9 +42,10 @@ __global__ void k_radon_out_T(DevGeom g, const float* __restrict__ sino, float* 
     const int j = i - k * nts;
     const float cth = __ldg(g.coarse_cos + j + nts / 2) * g.one_m_aR;
     const float sgn = flip ? -1.f : 1.f;
+    const float invN = 1.f / float(N);
     const float* in = sino + (size_t(b) * g.n_theta + i) * N;
     for (int c = threadIdx.x; c < N; c += blockDim.x) {
-        const float sp = sgn * float(2 * c - N) / float(N);
+        const float sp = sgn * float(2 * c - N) * invN;  // (x / N exactly for power-of-two N)
         const float rho = logf(fmaf(g.aR, sp, cth));
         const float t = (rho - g.log_ar) * g.inv_drho;
         const float kf = floorf(t);
