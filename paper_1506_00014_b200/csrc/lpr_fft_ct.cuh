@@ -177,6 +177,20 @@ __host__ __device__ constexpr bool band_keep(int r) {
     return BAND == 0 || r * NS < BAND || r * NS + NS - 1 > N / 2 - BAND;
 }
 
+// Padded walks: elements base + r STRIDE, r < R, of a buffer padded by
+// ct_pad<S> sit at ct_pad<S>(base) + r STRIDE + (r STRIDE >> S) whenever
+// STRIDE is a multiple of 2^S, or STRIDE = 1 with R dividing 2^S and base a
+// multiple of R (the walk stays inside one 2^S block). Then one padded base
+// per butterfly and compile-time offsets replace a shift-add per access.
+template <int S, int STRIDE, int R>
+__host__ __device__ constexpr bool pad_walk_ok() {
+    return S == 0 || STRIDE % (1 << S) == 0 || (STRIDE == 1 && (1 << S) % R == 0);
+}
+template <int S, int STRIDE>
+__host__ __device__ constexpr int pad_walk_off(int r) {
+    return r * STRIDE + (S ? (r * STRIDE) >> S : 0);
+}
+
 // One in-place pass of radix R at Stockham stride NS over a padded buffer.
 template <int N, int T, int S, int R, int NS, int OFF, bool INV, int BAND = 0, class TW>
 __device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, int tid) {
@@ -188,8 +202,14 @@ __device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, i
     for (int i = 0; i < NB; ++i) {
         const int b = tid + i * T;
         if (b < B) {
+            if constexpr (pad_walk_ok<S, B, R>()) {
+                const float2* xb = x + ct_pad<S>(b);
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[i][r] = x[ct_pad<S>(b + r * B)];
+                for (int r = 0; r < R; ++r) v[i][r] = xb[pad_walk_off<S, B>(r)];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[i][r] = x[ct_pad<S>(b + r * B)];
+            }
         }
     }
     __syncthreads();
@@ -207,9 +227,16 @@ __device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, i
             }
             Dft<R, INV>::run(v[i]);
             const int base = (b - k) * R + k;
+            if constexpr (pad_walk_ok<S, NS, R>()) {
+                float2* xw = x + ct_pad<S>(base);
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-                if (band_keep<N, R, NS, BAND>(r)) x[ct_pad<S>(base + r * NS)] = v[i][Dft<R, INV>::slot(r)];
+                for (int r = 0; r < R; ++r)
+                    if (band_keep<N, R, NS, BAND>(r)) xw[pad_walk_off<S, NS>(r)] = v[i][Dft<R, INV>::slot(r)];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (band_keep<N, R, NS, BAND>(r)) x[ct_pad<S>(base + r * NS)] = v[i][Dft<R, INV>::slot(r)];
+            }
         }
     }
     __syncthreads();
@@ -313,6 +340,7 @@ struct CtFft {
     // first radix, and the remaining passes for kernels that run the first
     // (twiddle-free, NS = 1) pass themselves straight from gathered registers
     static constexpr int kR1 = RadixPack<R...>::first;
+    static constexpr bool kPadWalk1 = pad_walk_ok<S, 1, kR1>();  // first-pass outputs bb R1 + r: one padded base
     template <bool INV>
     __device__ __forceinline__ static void run_tail(float2* x, const FftDesc& d, int gtid) {
         RadixPack<R...>::template tail<N, T, S, INV>(x, ct_tw(d), gtid);
@@ -489,6 +517,7 @@ struct RhoStream4 {
 
 struct GenericFft {
     static constexpr int kN = 0;
+    static constexpr bool kPadWalk1 = false;
     static constexpr int kT = 0;  // runtime: threads(d)
     static constexpr int kP = 1;
     static constexpr int kMinBlocks = 1;

@@ -541,8 +541,14 @@ __device__ __forceinline__ void first_pass_gathered(float2* sm, int tid, Gather&
                 }
             }
             Dft<R1, false>::run(v);
+            if constexpr (F::kPadWalk1) {  // the R1 outputs stay inside one padding block
+                float2* w = sm + F::idx(bb * R1);
 #pragma unroll
-            for (int r = 0; r < R1; ++r) sm[F::idx(bb * R1 + r)] = v[Dft<R1, false>::slot(r)];
+                for (int r = 0; r < R1; ++r) w[r] = v[Dft<R1, false>::slot(r)];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R1; ++r) sm[F::idx(bb * R1 + r)] = v[Dft<R1, false>::slot(r)];
+            }
         }
     }
     __syncthreads();
