@@ -41,13 +41,26 @@ struct FftDesc {
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
-// a * b = a.x (b.x, b.y) + a.y (-b.y, b.x)
+// a * b = a.x (b.x, b.y) + a.y (-b.y, b.x); the swizzled operand first and
+// the broadcast second, the order in which ptxas folds the swap / partial
+// negation and the broadcast into operand modifiers instead of MOVs
+#ifndef LPR_CMUL_SWZ_FIRST
+#define LPR_CMUL_SWZ_FIRST 1
+#endif
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+#if LPR_CMUL_SWZ_FIRST
+    return __ffma2_rn(make_float2(-b.y, b.x), make_float2(a.y, a.y), __fmul2_rn(b, make_float2(a.x, a.x)));
+#else
     return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), b));
+#endif
 }
 // a * conj(b) = a.x (b.x, -b.y) + a.y (b.y, b.x)
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+#if LPR_CMUL_SWZ_FIRST
+    return __ffma2_rn(make_float2(b.y, b.x), make_float2(a.y, a.y), __fmul2_rn(make_float2(b.x, -b.y), make_float2(a.x, a.x)));
+#else
     return __ffma2_rn(make_float2(a.y, a.y), make_float2(b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), make_float2(b.x, -b.y)));
+#endif
 }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 // multiply by -i (forward) or +i (inverse)

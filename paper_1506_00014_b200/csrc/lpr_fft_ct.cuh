@@ -67,7 +67,11 @@ LPR_WQ(32)
 
 // a * w for a (c, s, -s, c) entry
 __device__ __forceinline__ float2 cmul_q(float2 a, float4 w) {
+#if LPR_CMUL_SWZ_FIRST
+    return __ffma2_rn(make_float2(w.z, w.w), make_float2(a.y, a.y), __fmul2_rn(make_float2(w.x, w.y), make_float2(a.x, a.x)));
+#else
     return __ffma2_rn(make_float2(a.y, a.y), make_float2(w.z, w.w), __fmul2_rn(make_float2(a.x, a.x), make_float2(w.x, w.y)));
+#endif
 }
 
 // Composite radix R = P * Q in registers, natural order in and out:
@@ -177,6 +181,21 @@ __host__ __device__ constexpr bool band_keep(int r) {
     return BAND == 0 || r * NS < BAND || r * NS + NS - 1 > N / 2 - BAND;
 }
 
+// Shared-memory store of one complex value. ptxas otherwise copies many
+// packed-FP results into a fresh register pair before each STS.64 (two MOVs
+// per store in the rho FFT); the asm store takes the pair as it is.
+#ifndef LPR_STS_ASM
+#define LPR_STS_ASM 1
+#endif
+__device__ __forceinline__ void sts2(float2* p, float2 v) {
+#if LPR_STS_ASM
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(p))), "f"(v.x),
+                 "f"(v.y));
+#else
+    *p = v;
+#endif
+}
+
 // Padded walks: elements base + r STRIDE, r < R, of a buffer padded by
 // ct_pad<S> sit at ct_pad<S>(base) + r STRIDE + (r STRIDE >> S) whenever
 // STRIDE is a multiple of 2^S, or STRIDE = 1 with R dividing 2^S and base a
@@ -231,11 +250,11 @@ __device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, i
                 float2* xw = x + ct_pad<S>(base);
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    if (band_keep<N, R, NS, BAND>(r)) xw[pad_walk_off<S, NS>(r)] = v[i][Dft<R, INV>::slot(r)];
+                    if (band_keep<N, R, NS, BAND>(r)) sts2(xw + pad_walk_off<S, NS>(r), v[i][Dft<R, INV>::slot(r)]);
             } else {
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    if (band_keep<N, R, NS, BAND>(r)) x[ct_pad<S>(base + r * NS)] = v[i][Dft<R, INV>::slot(r)];
+                    if (band_keep<N, R, NS, BAND>(r)) sts2(x + ct_pad<S>(base + r * NS), v[i][Dft<R, INV>::slot(r)]);
             }
         }
     }
@@ -404,7 +423,7 @@ __device__ __forceinline__ void ct_mid_fused(float2* x, const TW* __restrict__ t
                 }
             } else {
 #pragma unroll
-                for (int r = 0; r < R; ++r) x[ct_pad<S>(R * b + r)] = u[Dft<R, true>::slot(r)];
+                for (int r = 0; r < R; ++r) sts2(x + ct_pad<S>(R * b + r), u[Dft<R, true>::slot(r)]);
             }
         }
     }

@@ -1268,6 +1268,7 @@ void launch_radon_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp
 }
 void launch_bp_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* img) {
     // (the sector loop unrolled for M = 3, all 12 tld4 gathers in flight: 1.107 -> 1.106)
+    // (taps of rows kt + 1, kt + 2 by direct loads beside two tld4 for rows kt - 1, kt: 1.105 -> 1.125)
     k_bp_out<<<dim3((g.N + 127) / 128, g.N, nb), 128, 0, st>>>(g, lp, img);
 }
 std::vector<float2> fft_pass_twiddles(int variant) {
