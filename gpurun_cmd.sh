@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-LPR_RHO_MSG=1 timeout 300 python scripts/stage_times.py 2048 16 > gpurun_out/st_msg.json 2>&1
+timeout 300 python scripts/stage_times.py 2048 16 > gpurun_out/st_dft.json 2>&1
+timeout 300 python scripts/stage_times.py 4096 4 > gpurun_out/st_dft4096.json 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest.txt

@@ -106,20 +106,19 @@ struct Dft<8, INV> {
         float2 o[4] = {v[1], v[3], v[5], v[7]};
         Dft<4, INV>::run(e);
         Dft<4, INV>::run(o);
-        // twiddles W8^k for k = 0..3
-        const float2 o1 = INV ? make_float2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
-                              : make_float2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+        // twiddles W8^k for k = 0..3; W8^1, W8^3 = h (1 -+ i) applied as
+        // e +- h u with u = o (1 -+ i) folded into FFMA2s
+        const float2 u1 = INV ? cadd(o[1], make_float2(-o[1].y, o[1].x)) : cadd(o[1], make_float2(o[1].y, -o[1].x));
         const float2 o2 = mul_mi<INV>(o[2]);
-        const float2 o3 = INV ? make_float2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
-                              : make_float2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+        const float2 u3 = INV ? csub(make_float2(-o[3].y, o[3].x), o[3]) : csub(make_float2(o[3].y, -o[3].x), o[3]);
         v[0] = cadd(e[0], o[0]);
         v[4] = csub(e[0], o[0]);
-        v[1] = cadd(e[1], o1);
-        v[5] = csub(e[1], o1);
+        v[1] = __ffma2_rn(u1, make_float2(h, h), e[1]);
+        v[5] = __ffma2_rn(u1, make_float2(-h, -h), e[1]);
         v[2] = cadd(e[2], o2);
         v[6] = csub(e[2], o2);
-        v[3] = cadd(e[3], o3);
-        v[7] = csub(e[3], o3);
+        v[3] = __ffma2_rn(u3, make_float2(h, h), e[3]);
+        v[7] = __ffma2_rn(u3, make_float2(-h, -h), e[3]);
     }
 };
 
@@ -178,11 +177,11 @@ struct Dft<3, INV> {
         const float2 t1 = cadd(v[1], v[2]);
         const float2 t2 = csub(v[1], v[2]);
         const float2 m = __ffma2_rn(t1, make_float2(-0.5f, -0.5f), v[0]);
-        const float2 u = INV ? __fmul2_rn(make_float2(-t2.y, t2.x), make_float2(s, s))
-                             : __fmul2_rn(make_float2(t2.y, -t2.x), make_float2(s, s));
+        // X1,2 = m +- s (-i t2) (forward): two FFMA2 on the swapped t2, no separate product
+        const float2 r = INV ? make_float2(-t2.y, t2.x) : make_float2(t2.y, -t2.x);
         v[0] = cadd(v[0], t1);
-        v[1] = cadd(m, u);
-        v[2] = csub(m, u);
+        v[1] = __ffma2_rn(r, make_float2(s, s), m);
+        v[2] = __ffma2_rn(r, make_float2(-s, -s), m);
     }
 };
 template <bool INV>
