@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-LPR_GPU_LIB=$PWD/paper_1506_00014_b200/liblpradon_gpu_p2.so timeout 300 python scripts/stage_times.py 2048 16 > gpurun_out/st_p2.json 2>&1
+for c in 8 16; do LPR_HOST_CHUNKS=$c timeout 600 python bench.py --no-cpu-baseline --steps 5 > gpurun_out/bench_hc$c.json 2> gpurun_out/bench_hc$c.err; done
