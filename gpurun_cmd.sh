@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-for c in 8 16; do LPR_HOST_CHUNKS=$c timeout 600 python bench.py --no-cpu-baseline --steps 5 > gpurun_out/bench_hc$c.json 2> gpurun_out/bench_hc$c.err; done
+timeout 300 python scripts/stage_times.py 2048 16 > gpurun_out/st_ld.json 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest.txt

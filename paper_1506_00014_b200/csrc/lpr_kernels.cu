@@ -489,6 +489,7 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
 // raster is the transposed one (element [c][r] = Q[r..r+3][c]) and a warp's
 // 32 consecutive samples again walk along raster rows.
 constexpr int kPitch2048 = 2048 + 2 * kApron;  // raster pitch of the N = 2048 plans (the bench size)
+constexpr int kNTheta2048 = 3072;              // their angle count (the Qg^T row stride)
 
 // SCALE = false leaves out the e^rho factor (constant along a column: the
 // fused kernel applies it to the column's spectrum instead of every sample).
@@ -919,7 +920,11 @@ __global__ void k_radon_out(DevGeom g, const float* __restrict__ lp, float* __re
 // Qg is stored s-major (Qg^T[b][s][theta], written by k_prefilter_sino_iir):
 // the 32 lanes of a warp take 32 consecutive lattice rows at nearly the same
 // s, so each tap load is one or two cache lines instead of 32.
-__device__ __forceinline__ float gather_sino(const float* __restrict__ row, int N, float t, int ld) {
+// LD > 0: the row stride (n_theta) at compile time, so the four tap rows are
+// load immediates off one address (the N = 2048 bench plan: 3072)
+template <int LD = 0>
+__device__ __forceinline__ float gather_sino(const float* __restrict__ row, int N, float t, int ld_rt) {
+    const int ld = LD ? LD : ld_rt;
     const float kf = floorf(t);
     float w[4];
     bsw(t - kf, w);
@@ -942,7 +947,7 @@ __device__ __forceinline__ float gather_sino(const float* __restrict__ row, int 
 // g(S_m^{-1}) on Omega_p (Alg. 2 step 3): theta' rows are polar rows, so each
 // sample is a 1-D spline along s (zero outside the detector), then the real
 // theta FFT of the zero-embedded doubled period.
-template <class F>
+template <class F, int LD = 0>
 __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                          const float* __restrict__ qg, float2* __restrict__ spec) {
     extern __shared__ float2 smem[];
@@ -966,8 +971,8 @@ __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, cons
                 const float* row = qg + size_t(b) * N * g.n_theta + i;
                 const float cth = __ldg(g.coarse_cos + jj) * g.one_m_aR;
                 const float sg = flip ? -halfN : halfN;
-                return make_float2(one ? gather_sino(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f,
-                                   two ? gather_sino(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f);
+                return make_float2(one ? gather_sino<LD>(row, N, fmaf((er0 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f,
+                                   two ? gather_sino<LD>(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f);
             });
             F::template run_tail<false>(sm, fd, G.tid);
             float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * g.n_rho;
@@ -1221,20 +1226,17 @@ __global__ void __launch_bounds__(256) k_radon_out_b(DevGeom g, const float* __r
         const float kf = floorf(t);
         float w[4];
         bsw(t - kf, w);
-        const int k0 = int(kf) - 1;
-        int idx[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int q = k0 + a;
-            idx[a] = q < 0 ? q + n : (q >= n ? q - n : q);
-        }
+        // t in [0, n] so k0 in [-1, n - 1]: only k0 = -1 wraps, and taps past
+        // n - 1 read the row's periodic copy of columns 0..2 (k_theta_inv)
+        int k0 = int(kf) - 1;
+        k0 = k0 < 0 ? k0 + n : k0;
 #pragma unroll
         for (int s = 0; s < SB; ++s) {
             if (s < ns) {
-                const float* row = srow + s * lps;
+                const float* row = srow + s * lps + k0;
                 float acc = 0.f;
 #pragma unroll
-                for (int a = 0; a < 4; ++a) acc = fmaf(w[a], row[idx[a]], acc);
+                for (int a = 0; a < 4; ++a) acc = fmaf(w[a], row[a], acc);
                 out[s * slice + c] = acc * g.out_scale;
             }
         }
@@ -1352,6 +1354,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
 #define COARSE(F)                                          \
     SET(k_theta_inv<F>, coarse.smem * coarse.per_block);    \
     SET(k_bp_theta_fwd<F>, coarse.smem * coarse.per_block); \
+    SET((k_bp_theta_fwd<F, kNTheta2048>), coarse.smem * coarse.per_block); \
     SET(k_theta_fwd_T<F>, coarse.smem * coarse.per_block)
     LPR_FFT_SWITCH(fine.variant, FINE)
     LPR_FFT_SWITCH(rho.variant, RHO)
@@ -1432,6 +1435,10 @@ void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevG
 
 void launch_bp_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                          const float* qg, float2* spec) {
+    if (L.variant == kFft2048 && g.n_theta == kNTheta2048) {
+        k_bp_theta_fwd<Fft2048, kNTheta2048><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qg, spec);
+        return;
+    }
 #define CALL(F) k_bp_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qg, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
