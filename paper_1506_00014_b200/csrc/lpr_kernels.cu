@@ -490,6 +490,7 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
 // 32 consecutive samples again walk along raster rows.
 constexpr int kPitch2048 = 2048 + 2 * kApron;  // raster pitch of the N = 2048 plans (the bench size)
 constexpr int kNTheta2048 = 3072;              // their angle count (the Qg^T row stride)
+constexpr int kNRho2048 = 4374;                // and their (7-smooth) N_rho
 
 // SCALE = false leaves out the e^rho factor (constant along a column: the
 // fused kernel applies it to the column's spectrum instead of every sample).
@@ -810,7 +811,9 @@ cudaError_t prepare_rho_pad() {
 
 // Hermitian theta inverse: two real columns per complex transform of length
 // 2 nts; rows [j0, j0 + win) of the periodic result are kept.
-template <class F>
+// NR, NTS > 0: N_rho and nts at compile time (the N = 2048 bench plan: 4374,
+// 1024), so row strides and the window geometry become immediates.
+template <class F, int NR = 0, int NTS = 0>
 __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                       const float2* __restrict__ spec, float* __restrict__ lp) {
     extern __shared__ float2 smem[];
@@ -820,14 +823,16 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
     const Slots sms{smem, E};
     const int m = blockIdx.y, b = blockIdx.z;
     const int l0b = 2 * P * blockIdx.x;
-    const int nts = g.nts, L2 = g.L2, n = g.n_rho;
+    const int nts = NTS ? NTS : g.nts, L2 = 2 * nts, n = NR ? NR : g.n_rho;
+    const int lps = NR ? (NR + 6) / 4 * 4 : g.lps;
+    const int win = NTS ? NTS + 8 : g.win, j0 = NTS ? -NTS / 2 - 4 : g.j0;
     const size_t item = size_t(b) * g.M + m;
     if (threadIdx.x < P) sms(threadIdx.x)[F::idx(nts)] = make_float2(0.f, 0.f);  // zeroed band edge
     load_packed_hermitian<F>(sms, spec + item * size_t(nts + 1) * n, nts, L2, n, l0b);
     __syncthreads();
     float2* res = F::template run<true>(sms(G.g), fft_scratch<F>(sms(G.g), fd), fd, G.tid);
     const Slots rs = result_slots<F>(smem, E, res);
-    float* out = lp + item * size_t(g.win) * g.lps;
+    float* out = lp + item * size_t(win) * lps;
     if constexpr (F::kT > 0) {
         // one column pair per thread, rows tid / P + j RS; the window rows
         // r < -j0 come from the top of the period (q + L2)
@@ -836,12 +841,12 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
         if (l < n) {
             const float2* src = rs(p);
             float* dst = out + l;
-            const bool pair = l + 1 < n && (reinterpret_cast<uintptr_t>(dst) & 7) == 0 && (g.lps % 2) == 0;
-            const int wrap = -g.j0;  // rows [0, wrap) read slot j0 + r + L2
-            for (int r = threadIdx.x / P; r < g.win; r += RS) {
-                const int q = g.j0 + r + (r < wrap ? L2 : 0);
+            const bool pair = l + 1 < n && (reinterpret_cast<uintptr_t>(dst) & 7) == 0 && (lps % 2) == 0;
+            const int wrap = -j0;  // rows [0, wrap) read slot j0 + r + L2
+            for (int r = threadIdx.x / P; r < win; r += RS) {
+                const int q = j0 + r + (r < wrap ? L2 : 0);
                 const float2 z = src[F::idx(q)];
-                float* d = dst + size_t(r) * g.lps;
+                float* d = dst + size_t(r) * lps;
                 if (pair) {
                     *reinterpret_cast<float2*>(d) = z;
                 } else {
@@ -1353,6 +1358,7 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
     if (rho.variant == kFft4374) SET(k_rho_stream<Rho4374>, rho_stream_smem(kFft4374));
 #define COARSE(F)                                          \
     SET(k_theta_inv<F>, coarse.smem * coarse.per_block);    \
+    SET((k_theta_inv<F, kNRho2048, 1024>), coarse.smem * coarse.per_block); \
     SET(k_bp_theta_fwd<F>, coarse.smem * coarse.per_block); \
     SET((k_bp_theta_fwd<F, kNTheta2048>), coarse.smem * coarse.per_block); \
     SET(k_theta_fwd_T<F>, coarse.smem * coarse.per_block)
@@ -1428,6 +1434,11 @@ void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGe
 
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                       const float2* spec, float* lp) {
+    if (L.variant == kFft2048 && g.n_rho == kNRho2048 && g.nts == 1024 && g.lps == (kNRho2048 + 6) / 4 * 4 &&
+        g.win == 1024 + 8 && g.j0 == -512 - 4) {
+        k_theta_inv<Fft2048, kNRho2048, 1024><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, spec, lp);
+        return;
+    }
 #define CALL(F) k_theta_inv<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, spec, lp)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
