@@ -952,7 +952,7 @@ __device__ __forceinline__ float gather_sino(const float* __restrict__ row, int 
 // g(S_m^{-1}) on Omega_p (Alg. 2 step 3): theta' rows are polar rows, so each
 // sample is a 1-D spline along s (zero outside the detector), then the real
 // theta FFT of the zero-embedded doubled period.
-template <class F, int LD = 0, int NR = 0>
+template <class F, int LD = 0>
 __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                          const float* __restrict__ qg, float2* __restrict__ spec) {
     extern __shared__ float2 smem[];
@@ -980,9 +980,8 @@ __global__ void LPR_LB(F) k_bp_theta_fwd(const __grid_constant__ DevGeom g, cons
                                    two ? gather_sino<LD>(row, N, fmaf((er1 - cth) * g.inv_aR, sg, halfN), g.n_theta) : 0.f);
             });
             F::template run_tail<false>(sm, fd, G.tid);
-            const int nr = NR ? NR : g.n_rho;  // compile-time row stride on the bench plan
-            float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * nr;
-            store_half_spectra<F>(Slots{smem, E}, L2, nts, nr, l0b, out);
+            float2* out = spec + (size_t(b) * g.M + m) * size_t(nts + 1) * g.n_rho;
+            store_half_spectra<F>(Slots{smem, E}, L2, nts, g.n_rho, l0b, out);
             return;
         }
     }
@@ -1362,7 +1361,6 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
     SET((k_theta_inv<F, kNRho2048, 1024>), coarse.smem * coarse.per_block); \
     SET(k_bp_theta_fwd<F>, coarse.smem * coarse.per_block); \
     SET((k_bp_theta_fwd<F, kNTheta2048>), coarse.smem * coarse.per_block); \
-    SET((k_bp_theta_fwd<F, kNTheta2048, kNRho2048>), coarse.smem * coarse.per_block); \
     SET(k_theta_fwd_T<F>, coarse.smem * coarse.per_block)
     LPR_FFT_SWITCH(fine.variant, FINE)
     LPR_FFT_SWITCH(rho.variant, RHO)
@@ -1448,11 +1446,6 @@ void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevG
 
 void launch_bp_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                          const float* qg, float2* spec) {
-    if (L.variant == kFft2048 && g.n_theta == kNTheta2048 && g.n_rho == kNRho2048) {
-        k_bp_theta_fwd<Fft2048, kNTheta2048, kNRho2048><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(
-            g, fd, qg, spec);
-        return;
-    }
     if (L.variant == kFft2048 && g.n_theta == kNTheta2048) {
         k_bp_theta_fwd<Fft2048, kNTheta2048><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qg, spec);
         return;
