@@ -152,6 +152,25 @@ STAGE_KERNELS = {
 }
 
 
+def ncu_lsu_pct(stage: str):
+    """L1/LSU data-pipe utilisation (% of peak) of `stage`'s kernel from the
+    latest committed ncu capture (profiles/*/ncu_dram_bytes.json), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_dram_bytes.json")), key=os.path.getmtime)
+    for path in reversed(files):
+        try:
+            with open(path) as f:
+                per = json.load(f).get("lsu_wavefronts_pct", {})
+        except Exception:
+            continue
+        kernels = STAGE_KERNELS.get(stage, ("k_" + stage,))
+        for name, v in per.items():
+            if any(name == k or name.startswith(k + "<") for k in kernels):
+                return v
+    return None
+
+
 def ncu_traffic(stage: str, slices: int):
     """dram__bytes_read + dram__bytes_write of `stage`'s kernel from the latest
     committed `ncu --set full` capture (profiles/*/ncu_dram_bytes.json, per
@@ -456,6 +475,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": dom["GBps"], "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["GBps"] / peak,
                          "traffic": traffic, "share_of_step": dom["share"],
+                         "l1_lsu_pct_ncu": ncu_lsu_pct(dom_name.split(":", 1)[1]),
                          "algorithmic_bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"]},
             "stages": stages,
             "clocks": clk.summary(),

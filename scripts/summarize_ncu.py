@@ -56,6 +56,7 @@ def main():
     ki = hdr.index("Kernel Name")
     lines = ["| kernel | " + " | ".join(KEYS.values()) + " |", "|" + "---|" * (len(KEYS) + 1)]
     traffic = {}
+    lsu = {}  # L1/LSU data-pipe utilisation: the bound of the gather / shared-FFT kernels
     seen = set()
     for d in data:
         name = short_name(d[ki])
@@ -73,12 +74,15 @@ def main():
             rd *= scale.get(units[hdr.index("dram__bytes_read.sum")], 1.0)
             wr *= scale.get(units[hdr.index("dram__bytes_write.sum")], 1.0)
             traffic[name] = (rd + wr) / slices
+            key = "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed"
+            if key in hdr:
+                lsu[name] = float(d[hdr.index(key)])
     with open(os.path.join(dst, "ncu_full_summary.md"), "w") as f:
         f.write(f"ncu --set full, {os.path.basename(rep)}; one R and one R# on {slices:g} slices at N=2048 "
                 "(scripts/profile_one.py), cold-cache replays.\n\n")
         f.write("\n".join(lines) + "\n")
     with open(os.path.join(dst, "ncu_dram_bytes.json"), "w") as f:
-        json.dump({"per_slice_bytes": traffic, "slices_per_launch": slices}, f, indent=1)
+        json.dump({"per_slice_bytes": traffic, "lsu_wavefronts_pct": lsu, "slices_per_launch": slices}, f, indent=1)
 
 
 if __name__ == "__main__":
