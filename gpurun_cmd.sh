@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 300 python scripts/stage_times.py 2048 16 > gpurun_out/st_pfs2.json 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest.txt

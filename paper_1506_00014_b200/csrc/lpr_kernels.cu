@@ -200,6 +200,9 @@ void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, c
 constexpr int kSRows = 128, kSCols = 64, kSP = kSCols + 2 * kIW + 1;  // odd pitch
 constexpr size_t kSinoPfSmem = size_t(kSRows) * kSP * sizeof(float);
 
+// LD > 0: n_theta (the Qg^T row stride) at compile time, so the transposed
+// store's column steps are immediates (the N = 2048 bench plan: 3072)
+template <int LD = 0>
 __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const float* __restrict__ sino,
                                                             float* __restrict__ qg) {
     extern __shared__ float s[];  // [kSRows][kSP]
@@ -232,19 +235,34 @@ __global__ void __launch_bounds__(128) k_prefilter_sino_iir(DevGeom g, const flo
     __syncthreads();
     // transposed store (Qg^T[b][s][theta], see gather_sino): a warp writes 32
     // consecutive theta of one s column; the odd pitch keeps the reads conflict-free
-    for (int idx = tid; idx < kSRows * kSCols; idx += 128) {
-        const int i = idx % kSRows, j = idx / kSRows;
-        if (i < rows && c0col + j < N) qg[(size_t(b) * N + c0col + j) * g.n_theta + i0 + i] = s[i * kSP + kIW + j];
+    // (128 threads = kSRows: thread i owns tile row i and steps the s column)
+    static_assert(kSRows == 128, "one tile row per thread");
+    if (tid < rows) {
+        const int ld = LD ? LD : g.n_theta;
+        float* d = qg + (size_t(b) * N + c0col) * ld + i0 + tid;
+        const float* src = s + tid * kSP + kIW;
+        const int cols = min(kSCols, N - c0col);
+#pragma unroll 8
+        for (int j = 0; j < cols; ++j) d[size_t(j) * ld] = src[j];
     }
 }
 
+constexpr int kNThetaSino = 3072;  // the N = 2048 plans' n_theta (k_prefilter_sino_iir<LD>)
+
 cudaError_t prepare_prefilter_sino() {
-    return cudaFuncSetAttribute(k_prefilter_sino_iir, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSinoPfSmem));
+    cudaError_t e = cudaFuncSetAttribute(k_prefilter_sino_iir<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSinoPfSmem));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_prefilter_sino_iir<kNThetaSino>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(kSinoPfSmem));
 }
 
 void launch_prefilter_sino(int nb, cudaStream_t st, const DevGeom& g, const float* sino, float* qg) {
-    k_prefilter_sino_iir<<<dim3((g.N + kSCols - 1) / kSCols, (g.n_theta + kSRows - 1) / kSRows, nb), 128, kSinoPfSmem,
-                           st>>>(g, sino, qg);
+    const dim3 grid((g.N + kSCols - 1) / kSCols, (g.n_theta + kSRows - 1) / kSRows, nb);
+    if (g.n_theta == kNThetaSino)
+        k_prefilter_sino_iir<kNThetaSino><<<grid, 128, kSinoPfSmem, st>>>(g, sino, qg);
+    else
+        k_prefilter_sino_iir<0><<<grid, 128, kSinoPfSmem, st>>>(g, sino, qg);
 }
 
 // ------------------------------------------------------------- FFT-policy kernels
