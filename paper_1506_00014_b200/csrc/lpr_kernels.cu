@@ -102,14 +102,16 @@ __device__ __forceinline__ void stage_rows(float* s, const float* __restrict__ s
     }
 }
 
-template <class T>
+// PITCH > 0: the raster pitch at compile time (N = 2048: 2056), so the store
+// loops' row steps are immediates
+template <class T, int PITCH = 0>
 __global__ void __launch_bounds__(128, 5) k_prefilter_2d_iir(DevGeom g, const float* __restrict__ img, T* __restrict__ q4,
                                                           T* __restrict__ q4t) {
     __shared__ float s[kIR][kICP];
     constexpr float z = -0.26794919243112270647f;
     constexpr float c0 = 6.0f / (1.0f - z), ca = -z / (1.0f - z);
     const int tid = threadIdx.x;
-    const int N = g.N, pitch = g.pitch;
+    const int N = g.N, pitch = PITCH ? PITCH : g.pitch;
     const int x0 = blockIdx.x * kIT, y0 = blockIdx.y * kIT, b = blockIdx.z;
     const float* src = img + size_t(b) * N * N;
     const int vx0 = x0 - kApron - kIW, vy0 = y0 - kApron - kIW;
@@ -187,7 +189,11 @@ void launch_prefilter_2d(bool quad, int nb, cudaStream_t st, const DevGeom& g, c
                          void* out_t) {
     const dim3 grid((g.pitch + kIT - 1) / kIT, (g.pitch + kIT - 1) / kIT, nb);
     if (quad)
-        k_prefilter_2d_iir<Tap><<<grid, 128, 0, st>>>(g, img, static_cast<Tap*>(out), static_cast<Tap*>(out_t));
+        if (g.pitch == 2048 + 2 * kApron)
+            k_prefilter_2d_iir<Tap, 2048 + 2 * kApron><<<grid, 128, 0, st>>>(g, img, static_cast<Tap*>(out),
+                                                                           static_cast<Tap*>(out_t));
+        else
+            k_prefilter_2d_iir<Tap><<<grid, 128, 0, st>>>(g, img, static_cast<Tap*>(out), static_cast<Tap*>(out_t));
     else
         k_prefilter_2d_iir<float><<<grid, 128, 0, st>>>(g, img, static_cast<float*>(out), nullptr);
 }
