@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 300 python scripts/stage_times.py 2048 16 > gpurun_out/st_pf2p.json 2>&1
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
