@@ -11,10 +11,16 @@ synthetic Shepp-Logan / random-disc slices, B * 16.8 MB > L2 per step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun every rank runs its shard; rank 0 prints one JSON line with
-the max-over-ranks device time. `--impl reference` times the CPU
-restatement of the reference path (oracle/, the reference's lp_ops is
-unimplemented upstream) on the host cores, rank 0 only.
+`--gpus N` > 1 outside torchrun re-executes the bench under
+`torch.distributed.run` with N ranks (one per GPU, NCCL). Every rank runs its
+shard; rank 0 prints one JSON line with the max-over-ranks device time, and
+`gathered` times the same step followed by a grouped NCCL send/recv of every
+rank's sinograms to rank 0 (the optional final gather).
+`--dry-run` runs that rank / shard / gather plumbing with gloo on CPU tensors
+(no GPU work, no measurement; the CPU test of the multi-rank path).
+`--impl reference` times the CPU restatement of the reference path
+(oracle/, the reference's lp_ops is unimplemented upstream) on the host
+cores, rank 0 only; it loads nothing from the product package.
 """
 from __future__ import annotations
 
@@ -41,23 +47,52 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=2048)
+    ap.add_argument("--size", dest="n", type=int, default=2048, help="image size N")
     ap.add_argument("--batch", type=int, default=16, help="slices per GPU per step")
     ap.add_argument("--plan", choices=["smooth", "default"], default="smooth",
                     help="smooth: N_rho rounded up to a 7-smooth FFT length; default: minimal N_rho")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-reps", type=int, default=5)
+    ap.add_argument("--dry-run", action="store_true", help="gloo on CPU: rank/shard/gather plumbing only")
+    ap.add_argument("--no-default-plan", action="store_true", help="skip the default-plan (minimal N_rho) row")
     return ap.parse_args()
+
+
+def relaunch(args) -> int:
+    """--gpus N outside torchrun: run this script under torch.distributed.run
+    with N ranks (127.0.0.1 rendezvous) and return its exit code."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def world():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def geometry(args):
+def smooth_at_least(n: int) -> int:
+    """Smallest length >= n whose factors are all in {2, 3, 5, 7}."""
+    while True:
+        m = n
+        for f in (2, 3, 5, 7):
+            while m % f == 0:
+                m //= f
+        if m == 1:
+            return n
+        n += 1
+
+
+def geometry(args, plan=None):
     import paper_1506_00014_b200 as lp
 
-    n_rho = lp.smooth_n_rho(args.n) if args.plan == "smooth" else 0
+    plan = plan or args.plan
+    n_rho = lp.smooth_n_rho(args.n) if plan == "smooth" else 0
     return lp.sampling_plan(args.n, 3, 0, n_rho)
 
 
@@ -152,43 +187,34 @@ STAGE_KERNELS = {
 }
 
 
-def ncu_lsu_pct(stage: str):
-    """L1/LSU data-pipe utilisation (% of peak) of `stage`'s kernel from the
-    latest committed ncu capture (profiles/*/ncu_dram_bytes.json), or None."""
+def _ncu_capture():
+    """The latest committed ncu summary (profiles/*/ncu_kernels.json): per kernel
+    the batch of the captured launch, its dram__bytes_read + write and its
+    L1/LSU data-pipe utilisation."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_dram_bytes.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_kernels.json")))
     for path in reversed(files):
         try:
             with open(path) as f:
-                per = json.load(f).get("lsu_wavefronts_pct", {})
+                return json.load(f), os.path.relpath(path, ROOT)
         except Exception:
             continue
-        kernels = STAGE_KERNELS.get(stage, ("k_" + stage,))
-        for name, v in per.items():
-            if any(name == k or name.startswith(k + "<") for k in kernels):
-                return v
-    return None
+    return None, None
 
 
-def ncu_traffic(stage: str, slices: int):
-    """dram__bytes_read + dram__bytes_write of `stage`'s kernel from the latest
-    committed `ncu --set full` capture (profiles/*/ncu_dram_bytes.json, per
-    slice), scaled to one launch of `slices` slices; None if not captured."""
-    import glob
-
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_dram_bytes.json")), key=os.path.getmtime)
-    for path in reversed(files):
-        try:
-            with open(path) as f:
-                per = json.load(f)["per_slice_bytes"]
-        except Exception:
-            continue
-        kernels = STAGE_KERNELS.get(stage, ("k_" + stage,))
-        for name, b in per.items():
-            if any(name == k or name.startswith(k + "<") for k in kernels):
-                return b * slices
-    return None
+def ncu_for(stage: str, batch: int):
+    """(traffic bytes per launch of `batch` slices, L1/LSU %, source) of the
+    kernel implementing `stage`, from one `ncu --set full` capture of the
+    bench-size launch; (None, None, None) when not captured."""
+    cap, src = _ncu_capture()
+    if not cap:
+        return None, None, None
+    kernels = STAGE_KERNELS.get(stage, ("k_" + stage,))
+    for name, rec in cap.get("kernels", {}).items():
+        if any(name == k or name.startswith(k + "<") for k in kernels):
+            return rec["dram_bytes"] * batch / rec["batch"], rec.get("lsu_pct"), src
+    return None, None, None
 
 
 def pcie_ceiling(h_img, d_img, d_sino, h_sino, nbytes_img, nbytes_sino, slices):
@@ -219,13 +245,22 @@ def pcie_ceiling(h_img, d_img, d_sino, h_sino, nbytes_img, nbytes_sino, slices):
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_sample(g, zeta, zeta_bp, slices: int = 1):
+def oracle_plan(args, plan=None):
+    """The bench plan built by the oracle alone (no product code loaded)."""
+    from oracle import lpo
+
+    p = lpo.make_plan(args.n, 3)
+    if (plan or args.plan) == "smooth":
+        p = lpo.make_plan(args.n, 3, 0, smooth_at_least(p.n_rho))
+    return p
+
+
+def cpu_sample(p, zeta, zeta_bp, slices: int = 1):
     """R then R# of `slices` slices through the oracle (fp64 CPU restatement,
     OpenMP over all host threads). Returns seconds per slice."""
     from oracle import lpo
 
-    p = lpo.make_plan(g.N, g.M, g.n_theta, g.n_rho)
-    f = lpo.phantom_image(g.N)
+    f = lpo.phantom_image(p.N)
     t = time.perf_counter()
     for _ in range(slices):
         s = lpo.fast_radon(p, zeta, f)
@@ -233,36 +268,40 @@ def cpu_sample(g, zeta, zeta_bp, slices: int = 1):
     return (time.perf_counter() - t) / slices
 
 
+CPU_SAMPLE = ("1 slice (Shepp-Logan, R then R#) per step of the same N=2048 plan; the reference's lp_ops is "
+              "unimplemented upstream, so this is the fp64 oracle restatement composed of blocks verified "
+              "bit-identical to the reference's compiled geometry/bspline/kernel code, OpenMP over all host "
+              "threads; plan constants (spectra) excluded")
+
+
 def run_reference(args):
+    """The reference arm: oracle/ only (lpo.make_plan, lpo.spectrum, Algorithms
+    1-2 in fp64), rank 0 of N; the other ranks exit without work."""
     rank, ws, _ = world()
     if rank != 0:
         return
-    import paper_1506_00014_b200 as lp
+    # all host threads (torchrun exports OMP_NUM_THREADS=1 to every rank; the
+    # oracle's OpenMP runtime reads it when oracle/liblpo.so is first loaded)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
+    from oracle import lpo
 
-    g = geometry(args)
-    z, zb = lp.zeta_spectrum(g), lp.zeta_bp_spectrum(g)  # plan constants, excluded from timing
+    p = oracle_plan(args)
+    z, zb = lpo.spectrum(p, 0), lpo.spectrum(p, 1)  # plan constants, excluded from timing
     cores = os.cpu_count()
-    warm = min(args.warmup, 1)
-    est = 0.0
+    warm = max(args.warmup, 3)
     for _ in range(warm):
-        est = cpu_sample(g, z, zb)
-    steps = args.steps
-    if est > 0:
-        steps = max(1, min(args.steps, int(150.0 / est)))
+        cpu_sample(p, z, zb)
     t = time.perf_counter()
-    for _ in range(steps):
-        cpu_sample(g, z, zb)
-    dt = (time.perf_counter() - t) / steps
+    for _ in range(args.steps):
+        cpu_sample(p, z, zb)
+    dt = (time.perf_counter() - t) / args.steps
     value = 1.0 / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": warm, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": config(args, g, 1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": "1 slice (R then R#) per step at the bench plan; the reference's lp_ops is "
-                                   "unimplemented upstream, so this is the fp64 oracle restatement composed of "
-                                   "blocks verified bit-identical to the reference's compiled geometry/bspline/"
-                                   "kernel code, OpenMP over all host threads"},
+        "dtype": "f64", "data": "synthetic", "config": config(args, p, ws),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": CPU_SAMPLE,
+                         "slices_per_step": 1},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -278,6 +317,8 @@ def run_ours(args):
     from paper_1506_00014_b200.sharding import stack_shard
 
     rank, ws, local = world()
+    if ws != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -326,9 +367,39 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = ws * B * args.steps / (ms / 1e3)
 
+    # the same step followed by the final gather of every rank's sinograms to
+    # rank 0 (grouped NCCL send/recv over NVLink; SURVEY.md §8(e) reports it as
+    # a separate row: rank 0's ingress bounds it, the sharded value does not)
+    gather_out = torch.empty(ws * B, g.n_theta, g.N, device=dev) if (rank == 0 and ws > 1) else None
+
+    def gathered_step():
+        step()
+        sharding.gather_to_root(sino, 0, gather_out)
+
+    for _ in range(2):
+        gathered_step()
+    torch.cuda.synchronize()
+    barrier()
+    ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ga.record(stream)
+    g_steps = max(2, min(args.steps, 10))
+    for _ in range(g_steps):
+        gathered_step()
+    gb.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_g = max_over_ranks(ga.elapsed_time(gb)) / g_steps
+    sino_bytes = B * g.n_theta * g.N * 4
+    gathered = {"value": ws * B / (ms_g / 1e3), "unit": UNIT, "ms_per_step": ms_g, "steps": g_steps,
+                "bytes_to_rank0_per_step": (ws - 1) * sino_bytes,
+                "how": "step + torch batch_isend_irecv (grouped ncclSend/ncclRecv) of every rank's "
+                       f"{B} sinograms to rank 0, device events, max over ranks"}
+    del gather_out
+
     # R-only / R#-only throughput (same buffers, device events)
-    def timed(fn, n=5):
-        fn()
+    def timed(fn, n=5, warm=1):
+        for _ in range(warm):
+            fn()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
@@ -433,29 +504,54 @@ def run_ours(args):
     # dominant kernel against the measured HBM copy bandwidth
     prof_r = roofline.profile_stages(plan, "radon", imgs.data_ptr(), sino.data_ptr(), B, args.profile_reps)
     prof_b = roofline.profile_stages(plan, "backproject", sino.data_ptr(), back.data_ptr(), B, args.profile_reps)
-    by_r = roofline.stage_bytes(g, "radon", B)
-    by_b = roofline.stage_bytes(g, "backproject", B)
+    peak, peak_kind = measured_peak()
     stages = {}
-    for op, prof, by in (("R", prof_r, by_r), ("R#", prof_b, by_b)):
+    for op, name, prof in (("R", "radon", prof_r), ("R#", "backproject", prof_b)):
+        by, comp = roofline.stage_bytes(g, name, B), roofline.compulsory_bytes(g, name, B)
         for k, v in prof.items():
-            stages[f"{op}:{k}"] = {"ms": v, "bytes": by[k], "GBps": by[k] / (v * 1e-3) / 1e9}
+            tr, lsu, src = ncu_for(k, B)
+            stages[f"{op}:{k}"] = {"ms": v, "bytes": by[k], "GBps": by[k] / (v * 1e-3) / 1e9,
+                                   "frac": by[k] / (v * 1e-3) / 1e9 / peak,
+                                   "compulsory_bytes": comp[k],
+                                   "frac_compulsory": comp[k] / (v * 1e-3) / 1e9 / peak,
+                                   "traffic": tr, "traffic_over_bytes": (tr / by[k]) if tr else None,
+                                   "l1_lsu_pct_ncu": lsu}
     total = sum(s["ms"] for s in stages.values())
     dom_name, dom = max(stages.items(), key=lambda kv: kv[1]["ms"])
-    peak, peak_kind = measured_peak()
-    traffic = ncu_traffic(dom_name.split(":", 1)[1], B)
     for s in stages.values():
         s["share"] = s["ms"] / total
-        s["frac"] = s["GBps"] / peak
+    ncu_src = _ncu_capture()[1]
+
+    # the reference's own sampling_plan (minimal N_rho, 4333 = 7 * 619 at
+    # N=2048: its rho convolution runs zero-padded over 8748) on the same stack
+    default_plan = None
+    if args.plan == "smooth" and not args.no_default_plan:
+        gd = geometry(args, "default")
+        pd = lp.RadonPlan(gd, max_batch=B, device=local)
+        hd = pd.handle
+        sino_d = torch.empty(B, gd.n_theta, gd.N, device=dev)
+
+        def step_d():
+            lp._lib.check(L.lpr_gpu_radon(hd, imgs.data_ptr(), sino_d.data_ptr(), B, sp))
+            lp._lib.check(L.lpr_gpu_backproject(hd, sino_d.data_ptr(), back.data_ptr(), B, sp))
+
+        ms_d = timed(step_d, n=max(3, min(args.steps, 10)), warm=3)
+        prof_d = roofline.profile_stages(pd, "radon", imgs.data_ptr(), sino_d.data_ptr(), B, 2)
+        prof_db = roofline.profile_stages(pd, "backproject", sino_d.data_ptr(), back.data_ptr(), B, 2)
+        default_plan = {"n_rho": gd.n_rho, "value": ws * B / (ms_d / 1e3), "unit": UNIT, "ms_per_step": ms_d,
+                        "stages_ms": {**{f"R:{k}": v for k, v in prof_d.items()},
+                                      **{f"R#:{k}": v for k, v in prof_db.items()}}}
+        del sino_d
+        pd.close()
 
     result = None
     if rank == 0:
         cpu = None
         if ws == 1 and not args.no_cpu_baseline:
             try:
-                sec = cpu_sample(g, z, zb)
+                sec = cpu_sample(oracle_plan(args), z, zb)
                 cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                       "sample": "1 slice of the same workload (Shepp-Logan, R then R#) through the fp64 oracle "
-                                 "restatement with OpenMP on all host threads; plan constants excluded"}
+                       "sample": CPU_SAMPLE, "slices": 1}
             except Exception as e:  # the CPU leg is a reported baseline, not the product
                 cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                        "sample": f"unavailable: {e}"}
@@ -473,11 +569,17 @@ def run_ours(args):
                     "sequential_value": e2e_seq_value, **link},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": dom["GBps"], "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["GBps"] / peak,
-                         "traffic": traffic, "share_of_step": dom["share"],
-                         "l1_lsu_pct_ncu": ncu_lsu_pct(dom_name.split(":", 1)[1]),
-                         "algorithmic_bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"]},
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["frac"],
+                         "traffic": dom["traffic"], "share_of_step": dom["share"],
+                         "l1_lsu_pct_ncu": dom["l1_lsu_pct_ncu"], "ncu_source": ncu_src,
+                         "algorithmic_bytes_per_launch": dom["bytes"],
+                         "bytes_model": "SURVEY.md §8(d) (fused kernels: sum of their stages)",
+                         "frac_compulsory": dom["frac_compulsory"], "ms_per_launch": dom["ms"],
+                         "step_frac": (roofline.slice_bytes(g, "radon") + roofline.slice_bytes(g, "backproject"))
+                         * B / (ms_step * 1e-3) / 1e9 / peak},
             "stages": stages,
+            "gathered": gathered,
+            "default_plan": default_plan,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -489,9 +591,52 @@ def run_ours(args):
     return result
 
 
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing of run_ours on CPU with gloo, no GPU
+    and no measurement: world/--gpus check, slice sharding, max-over-ranks,
+    and the final gather of every rank's (stand-in) sinograms to rank 0,
+    verified element by element. Rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1506_00014_b200 import sharding
+
+    rank, ws, _ = world()
+    if ws != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    if ws > 1:
+        dist.init_process_group("gloo")
+    B, n_theta, N = args.batch, 3 * args.n // 2, args.n
+    start, count = sharding.stack_shard(B * ws, ws, rank)
+    sino = torch.arange(start, start + count, dtype=torch.float32).reshape(-1, 1, 1).expand(count, n_theta, N)
+    sino = sino.contiguous()
+    slowest = sharding.max_over_ranks(float(rank))
+    out = sharding.gather_to_root(sino, 0)
+    line = None
+    if rank == 0:
+        ok = out is not None and out.shape[0] == B * ws and all(
+            bool((out[i] == i).all()) for i in range(B * ws))
+        line = {"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": ws, "dry_run": True, "backend": "gloo",
+                "config": {"N": N, "n_theta": n_theta, "global_batch": B * ws,
+                           "parallelism": f"slices sharded dp{ws}"},
+                "gathered": {"bytes_to_rank0_per_step": (ws - 1) * B * n_theta * N * 4, "verified": ok},
+                "max_over_ranks": slowest}
+        print(json.dumps(line), flush=True)
+        if not ok:
+            raise SystemExit("dry run: gather mismatch")
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

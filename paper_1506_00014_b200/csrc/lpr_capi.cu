@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <complex>
+#include <mutex>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -24,7 +25,6 @@ void spectrum_gpu(int device, const lpr_geometry& g, int kind, double* out);
 void rho_pad_multipliers(int device, int rows, int n, int nb, const double* mult, float2* d_out);
 
 // kernels (lpr_kernels.cu, lpr_transpose.cu)
-__global__ void k_radon_out(DevGeom g, const float* lp, float* sino);
 __global__ void k_radon_out_T(DevGeom g, const float* sino, float* lp);
 __global__ void k_prefilter_cols_T(DevGeom g, const float* band, int H, const float* qbar, float* tmp);
 __global__ void k_prefilter_rows_T(DevGeom g, const float* band, int H, const float* tmp, float* img, float scale);
@@ -128,24 +128,27 @@ struct lpr_gpu_plan {
     int band_h = 0;
     float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
     Tap* q4 = nullptr;  // coefficient raster read by the R gather; qf aliases it as the R^T scatter target
-    Tap* q4t = nullptr; // transposed quad raster for sector 0 (LPR_Q4T=0: none)
-    bool q4t_on = true;
+    Tap* q4t = nullptr; // transposed quad raster for sector 0
     float2* spec = nullptr;
     float *d_in = nullptr, *d_out = nullptr;   // staging for the *_host entry points
     float *h_in = nullptr, *h_out = nullptr;   // pinned
     cudaStream_t stream = nullptr;
     cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams
-    cudaStream_t s_aux = nullptr;                   // second half batch (run_split)
-    cudaEvent_t ev_split[3] = {};
-    int host_chunks = 16;                           // pipeline depth of the pinned host path (LPR_HOST_CHUNKS; 4/8/16 measured 684/798/813 e2e)
-    bool split = false;                             // LPR_SPLIT=1: two staggered half batches (measured slower)
+    static constexpr int kHostChunks = 16;          // pipeline depth of the pinned host path (4/8/16 measured 684/798/813 e2e)
+    // Calls share the scratch above, so they are serialised: the mutex covers
+    // the host side of a call (enqueue, host staging), and ev_done, recorded on
+    // the stream of the call that last used the scratch, orders its device work
+    // before the next call's (which may come on another stream).
+    std::recursive_mutex mu;
+    cudaEvent_t ev_done = nullptr;
+    bool has_done = false;
     static constexpr int kHostSlots = 4;  // device staging slots of the pinned host pipeline
     cudaEvent_t ev_h2d[kHostSlots] = {}, ev_comp[kHostSlots] = {}, ev_d2h[kHostSlots] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     bool tex_gather = false;      // LPR_PLAN_TEXTURE_GATHER ablation
     int tex_mode = 0;             // gather path of the R fine grid: 0 quad taps, 1 hardware bilinear (ablation)
     cudaTextureObject_t qtex = 0;
-    cudaTextureObject_t lptex = 0;  // tld4 view of lp for the R# output resampling (LPR_BP_TEX=0: direct loads)
+    cudaTextureObject_t lptex = 0;  // tld4 view of lp for the R# output resampling (0: direct loads)
     std::vector<void*> allocs;
     long long launches = 0, ffts = 0;
     // EM state (allocated on first use): Rf / ratio sinograms, R# images, the
@@ -210,10 +213,7 @@ struct lpr_gpu_plan {
         launch = fft_launch_config(d);
         if (launch.variant != kFftGeneric) d.twp = upload(fft_pass_twiddles(launch.variant));
         // rho pass: the TMA-streamed kernel where one exists for this length
-        // (LPR_RHO_STREAM=0 selects the one-block-per-row kernel, for A/B runs)
-        const char* rs = std::getenv("LPR_RHO_STREAM");
-        if (staged_row && rho_stream_smem(launch.variant) > 0 && (n * sizeof(float2)) % 16 == 0 &&
-            !(rs && rs[0] == '0')) {
+        if (staged_row && rho_stream_smem(launch.variant) > 0 && (n * sizeof(float2)) % 16 == 0) {
             d.twp_sfwd = upload(rho_stream_fwd_twiddles(launch.variant));
             d.twp_inv = upload(rho_stream_inv_twiddles(launch.variant));
             launch.rho_stream = 1;
@@ -234,9 +234,7 @@ struct lpr_gpu_plan {
             if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
             if (ev_d2h[i]) cudaEventDestroy(ev_d2h[i]);
         }
-        for (auto& e : ev_split)
-            if (e) cudaEventDestroy(e);
-        if (s_aux) cudaStreamDestroy(s_aux);
+        if (ev_done) cudaEventDestroy(ev_done);
         if (s_in) cudaStreamDestroy(s_in);
         if (s_out) cudaStreamDestroy(s_out);
         if (stream) cudaStreamDestroy(stream);
@@ -271,7 +269,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     g.Lf = 2 * g.nf;
     g.L2 = 2 * G.nts;
     g.win = G.nts + 8;
-    g.lps = (G.n_rho + 3 + 7) / 8 * 8;  // + 3 periodic columns (k_theta_inv), rounded to 32 bytes (texture pitch)
+    g.lps = lp_stride(G.n_rho);
     g.j0 = -G.nts / 2 - 4;
     g.pitch = G.N + 2 * kApron;
     g.aR = float(G.a_R);
@@ -356,12 +354,11 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     p->mult_RT = p->upload(mr);
     // non-7-smooth N_rho with a compile-time padded plan: the rho pass runs as a
     // zero-padded linear convolution (k_rho_pad) with these padded multipliers
-    const char* pe = std::getenv("LPR_RHO_PAD");
-    p->rho_pad = (p->l_rho.variant == kFftGeneric && !(pe && pe[0] == '0')) ? int(rho_pad_length(int(nr))) : 0;
+    p->rho_pad = p->l_rho.variant == kFftGeneric ? int(rho_pad_length(int(nr))) : 0;
     // N_rho equal to the padded plan's length (8748: the N = 4096 bench plan):
     // the same compile-time kernel runs the circular convolution directly with
     // the plain multipliers (no padding)
-    p->rho_direct = p->l_rho.variant == kFftGeneric && !(pe && pe[0] == '0') && rho_direct_length() == size_t(nr);
+    p->rho_direct = p->l_rho.variant == kFftGeneric && rho_direct_length() == size_t(nr);
     if (p->rho_direct) ck(prepare_rho_pad(), "rho pad smem attribute");
     if (p->rho_pad) {
         const long rr = nts + 1, nb = p->rho_pad;
@@ -457,7 +454,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     const size_t B = size_t(p->max_batch);
     p->tmp = p->dalloc<float>(B * G.N * g.pitch);
     p->q4 = p->dalloc<Tap>(B * g.pitch * g.pitch);
-    if (p->q4t_on && p->tex_mode == 0) p->q4t = p->dalloc<Tap>(B * g.pitch * g.pitch);
+    if (p->tex_mode == 0) p->q4t = p->dalloc<Tap>(B * g.pitch * g.pitch);
     p->qf = reinterpret_cast<float*>(p->q4);
     p->qg = p->dalloc<float>(B * G.n_theta * G.N);
     p->fsino = p->dalloc<float>(B * G.n_theta * G.N);
@@ -471,14 +468,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking), "cudaStreamCreate");
-    ck(cudaStreamCreateWithFlags(&p->s_aux, cudaStreamNonBlocking), "cudaStreamCreate");
-    for (auto& e : p->ev_split) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-    {
-        const char* hc = std::getenv("LPR_HOST_CHUNKS");
-        if (hc && std::atoi(hc) > 0) p->host_chunks = std::atoi(hc);
-        const char* sp = std::getenv("LPR_SPLIT");
-        p->split = sp && sp[0] == '1';
-    }
+    ck(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming), "cudaEventCreate");
     for (int i = 0; i < lpr_gpu_plan::kHostSlots; ++i) {
         ck(cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming), "cudaEventCreate");
@@ -515,12 +505,11 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         // R# output resampling taps through the texture path (four exact tld4
         // gathers per sample instead of 16 scalar loads; measured 1.51 -> 1.11 ms
         // per 16 slices), when the window buffer fits one pitched 2-D texture
-        const char* bt = std::getenv("LPR_BP_TEX");
         const size_t h = size_t(B) * G.M * g.win;
         int max_h = 0, max_w = 0;
         ck(cudaDeviceGetAttribute(&max_h, cudaDevAttrMaxTexture2DLinearHeight, p->device), "device query");
         ck(cudaDeviceGetAttribute(&max_w, cudaDevAttrMaxTexture2DLinearWidth, p->device), "device query");
-        if (!(bt && bt[0] == '0') && h <= size_t(max_h) && g.lps <= max_w) {
+        if (h <= size_t(max_h) && g.lps <= max_w) {
             cudaResourceDesc rd{};
             rd.resType = cudaResourceTypePitch2D;
             rd.res.pitch2D.devPtr = p->lp;
@@ -556,87 +545,70 @@ void rho_chunk(lpr_gpu_plan* p, int which, int nb, cudaStream_t st, const DevGeo
     launch_rho_pass(p->l_rho, grid, st, g, p->d_rho, which == 0 ? p->mult_R : which == 1 ? p->mult_B : p->mult_RT, spec);
 }
 
+// One call on a plan. Calls share the plan's scratch, so they are serialised
+// (ADVICE r1): the plan mutex is held for the whole host side of the call, and
+// the call's stream first waits for the device work of the previous call
+// (ev_done, recorded on whichever stream that call used), so a device call on
+// a user stream and a host call on the plan's own stream cannot overlap on
+// the same buffers.
+struct Call {
+    lpr_gpu_plan* p;
+    cudaStream_t st;
+    std::unique_lock<std::recursive_mutex> lk;
+    Call(lpr_gpu_plan* plan, cudaStream_t s) : p(plan), st(s), lk(plan->mu) {
+        ck(cudaSetDevice(p->device), "cudaSetDevice");
+        if (p->has_done) ck(cudaStreamWaitEvent(st, p->ev_done, 0), "cudaStreamWaitEvent");
+    }
+    ~Call() {
+        if (cudaEventRecord(p->ev_done, st) == cudaSuccess) p->has_done = true;
+    }
+};
+
 // Optional per-stage profiling: when p->prof is set, an event is recorded
 // before the first and after every launch (lpr_gpu_profile_stages).
 inline void mark(lpr_gpu_plan* p, int i, cudaStream_t st) {
     if (p->prof) ck(cudaEventRecord(p->prof[i], st), "profile event");
 }
 
-// The plan's per-slice scratch seen from slice b0 on (two concurrent half
-// batches use disjoint slices of it, run_device); `after_first`, when set, is
-// recorded after the first launch (the other half starts its chain there).
-struct Scratch {
-    Tap *q4, *q4t;
-    float *qg, *fsino, *lp;
-    float2* spec;
-    DevGeom g;
-    cudaEvent_t after_first = nullptr;
-};
-
-Scratch scratch(lpr_gpu_plan* p, int b0) {
+void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
     const DevGeom& g = p->g;
-    Scratch s{};
-    s.q4 = p->q4 + size_t(b0) * g.pitch * g.pitch;
-    s.q4t = p->q4t ? p->q4t + size_t(b0) * g.pitch * g.pitch : nullptr;
-    s.qg = p->qg + size_t(b0) * g.n_theta * g.N;
-    s.fsino = p->fsino + size_t(b0) * g.n_theta * g.N;
-    s.lp = p->lp + size_t(b0) * g.M * g.win * size_t(g.lps);
-    s.spec = p->spec + size_t(b0) * g.M * size_t(g.nts + 1) * g.n_rho;
-    s.g = g;
-    s.g.sb0 = b0;
-    return s;
-}
-
-inline void first_done(const Scratch& s, cudaStream_t st) {
-    if (s.after_first) ck(cudaEventRecord(s.after_first, st), "event");
-}
-
-void radon_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* img, float* sino, int nb, cudaStream_t st) {
-    const DevGeom& g = S.g;
     mark(p, 0, st);
-    launch_prefilter_2d(p->tex_mode == 0, nb, st, g, img, S.q4, S.q4t);
-    first_done(S, st);
+    launch_prefilter_2d(p->tex_mode == 0, nb, st, g, img, p->q4, p->q4t);
     mark(p, 1, st);
-    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, S.q4, S.q4t, S.spec,
+    launch_radon_theta_fwd(p->l_fine, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_fine, p->q4, p->q4t, p->spec,
                            p->tex_mode);
     mark(p, 2, st);
-    rho_chunk(p, 0, nb, st, g, S.spec);
+    rho_chunk(p, 0, nb, st, g, p->spec);
     mark(p, 3, st);
-    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.spec, S.lp);
+    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->spec, p->lp);
     mark(p, 4, st);
-    launch_radon_out(nb, st, g, S.lp, sino);
+    launch_radon_out(nb, st, g, p->lp, sino);
     mark(p, 5, st);
     check_launch("radon launch");
     p->launches += 5;
     p->ffts += 2LL * g.M * nb;
 }
-void radon_chunk(lpr_gpu_plan* p, const float* img, float* sino, int nb, cudaStream_t st) {
-    radon_chunk_s(p, scratch(p, 0), img, sino, nb, st);
-}
 const char* const kRadonStages[] = {"prefilter_2d", "radon_theta_fwd", "rho_pass", "theta_inv", "radon_out"};
 
-void backproject_chunk_s(lpr_gpu_plan* p, const Scratch& S, const float* sino, float* img, int nb, cudaStream_t st) {
-    const DevGeom& g = S.g;
+void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
+    const DevGeom& g = p->g;
     mark(p, 0, st);
-    launch_prefilter_sino(nb, st, g, sino, S.qg);
-    first_done(S, st);
+    launch_prefilter_sino(nb, st, g, sino, p->qg);
     mark(p, 1, st);
-    launch_bp_theta_fwd(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.qg, S.spec);
+    launch_bp_theta_fwd(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->qg, p->spec);
     mark(p, 2, st);
-    rho_chunk(p, 1, nb, st, g, S.spec);
+    rho_chunk(p, 1, nb, st, g, p->spec);
     mark(p, 3, st);
-    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, S.spec, S.lp);
+    launch_theta_inv(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->spec, p->lp);
     mark(p, 4, st);
-    launch_bp_out(nb, st, g, S.lp, img);
+    launch_bp_out(nb, st, g, p->lp, img);
     mark(p, 5, st);
     check_launch("backprojection launch");
     p->launches += 5;
     p->ffts += 2LL * g.M * nb;
 }
-void backproject_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
-    backproject_chunk_s(p, scratch(p, 0), sino, img, nb, st);
-}
 void transpose_chunk(lpr_gpu_plan* p, const float* sino, float* img, int nb, cudaStream_t st) {
+    if (p->tex_gather) throw std::invalid_argument("radon_transpose: not defined for a texture-gather plan");
     const DevGeom& g = p->g;
     k_radon_out_T<<<dim3(g.n_theta, nb), 256, g.n_rho * sizeof(float), st>>>(g, sino, p->lp);
     launch_theta_fwd_T(p->l_coarse, dim3(cdiv(g.n_rho, 2), g.M, nb), st, g, p->d_coarse, p->lp, p->spec);
@@ -680,6 +652,7 @@ void em_buffers(lpr_gpu_plan* p) {
     p->em_bad = p->dalloc<int>(1);
     // sensitivity R# chi_C: chi_C = 1 on every bin (|s| <= 1/2 covers the detector)
     cudaStream_t st = p->stream;
+    if (p->has_done) ck(cudaStreamWaitEvent(st, p->ev_done, 0), "cudaStreamWaitEvent");  // the scratch is free
     launch_fill(p->em_rf, size_t(G.n_theta) * G.N, 1.f, st);
     backproject_chunk(p, p->em_rf, p->em_bp, 1, st);
     launch_slice_max(p->em_bp, size_t(G.N) * G.N, 1, p->em_gmax, p->em_bad, st);
@@ -711,37 +684,16 @@ void em_chunk(lpr_gpu_plan* p, const float* g, float* f, int nb, int iters, doub
 
 using ChunkFn = void (*)(lpr_gpu_plan*, const float*, float*, int, cudaStream_t);
 
-using ChunkSFn = void (*)(lpr_gpu_plan*, const Scratch&, const float*, float*, int, cudaStream_t);
-
-// Two half batches on two streams, the second starting once the first has
-// finished its first kernel: the halves then run different stages side by
-// side (a gather-bound theta kernel next to an FMA-bound rho pass, ...).
-void run_split(lpr_gpu_plan* p, ChunkSFn fn, const float* in, float* out, int nb, size_t in_sz, size_t out_sz,
-               cudaStream_t st) {
-    const int ha = (nb + 1) / 2, hb = nb - ha;
-    Scratch A = scratch(p, 0), B = scratch(p, ha);
-    A.after_first = p->ev_split[0];
-    ck(cudaEventRecord(p->ev_split[1], st), "event");  // B's inputs are ready when st gets here
-    fn(p, A, in, out, ha, st);
-    ck(cudaStreamWaitEvent(p->s_aux, p->ev_split[1], 0), "wait");
-    ck(cudaStreamWaitEvent(p->s_aux, p->ev_split[0], 0), "wait");
-    fn(p, B, in + size_t(ha) * in_sz, out + size_t(ha) * out_sz, hb, p->s_aux);
-    ck(cudaEventRecord(p->ev_split[2], p->s_aux), "event");
-    ck(cudaStreamWaitEvent(st, p->ev_split[2], 0), "wait");
-}
-
 void run_device(lpr_gpu_plan* p, ChunkFn fn, const float* in, float* out, int batch, size_t in_sz, size_t out_sz,
-                void* stream, ChunkSFn sfn = nullptr) {
+                void* stream) {
     if (!p) throw std::invalid_argument("null plan");
     if (batch < 0 || (batch > 0 && (!in || !out))) throw std::invalid_argument("bad buffers or batch");
     ck(cudaSetDevice(p->device), "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const Call call(p, st);
     for (int b0 = 0; b0 < batch; b0 += p->max_batch) {
         const int nb = std::min(p->max_batch, batch - b0);
-        if (sfn && p->split && nb >= 2 && !p->prof)
-            run_split(p, sfn, in + size_t(b0) * in_sz, out + size_t(b0) * out_sz, nb, in_sz, out_sz, st);
-        else
-            fn(p, in + size_t(b0) * in_sz, out + size_t(b0) * out_sz, nb, st);
+        fn(p, in + size_t(b0) * in_sz, out + size_t(b0) * out_sz, nb, st);
     }
 }
 
@@ -765,9 +717,10 @@ void run_host(lpr_gpu_plan* p, ChunkFn fn, const float* hin, float* hout, int ba
     ck(cudaSetDevice(p->device), "cudaSetDevice");
     const bool pin_in = is_pinned(hin), pin_out = is_pinned(hout);
     cudaStream_t st = p->stream;
+    const Call call(p, st);
     if (pin_in && pin_out && batch > 1 && p->max_batch > 1) {
         // ~8 chunks: the exposed pipeline fill (first H2D) and drain (last D2H) shrink with the chunk
-        const int c = std::max(1, std::min(p->max_batch / 2, (batch + p->host_chunks - 1) / p->host_chunks));
+        const int c = std::max(1, std::min(p->max_batch / 2, (batch + lpr_gpu_plan::kHostChunks - 1) / lpr_gpu_plan::kHostChunks));
         const int chunks = (batch + c - 1) / c;
         // up to kHostSlots chunks in flight: a copy waits only for the compute
         // (or D2H) of the chunk kHostSlots back, so jitter from other work on
@@ -868,8 +821,6 @@ int lpr_gpu_plan_create_ex(int device, const lpr_geometry* geom, const double* z
         p->max_batch = max_batch;
         p->tex_gather = (flags & LPR_PLAN_TEXTURE_GATHER) != 0;
         p->tex_mode = p->tex_gather ? 1 : 0;
-        const char* qt = std::getenv("LPR_Q4T");
-        p->q4t_on = !(qt && qt[0] == '0');
         try {
             init_plan(p, zeta, zeta_bp);
         } catch (...) {
@@ -886,8 +837,9 @@ int lpr_gpu_sensitivity(lpr_gpu_plan* p, float* d_img, void* stream) {
     return guard([&] {
         if (!p || !d_img) throw std::invalid_argument("null argument");
         ck(cudaSetDevice(p->device), "cudaSetDevice");
-        em_buffers(p);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const Call call(p, st);
+        em_buffers(p);
         launch_fill(p->em_rf, size_t(p->geo.n_theta) * p->geo.N, 1.f, st);
         backproject_chunk(p, p->em_rf, d_img, 1, st);
         check_launch("sensitivity");
@@ -898,8 +850,9 @@ int lpr_gpu_sensitivity_host(lpr_gpu_plan* p, float* h_img) {
     return guard([&] {
         if (!p || !h_img) throw std::invalid_argument("null argument");
         ck(cudaSetDevice(p->device), "cudaSetDevice");
-        em_buffers(p);
         cudaStream_t st = p->stream;
+        const Call call(p, st);
+        em_buffers(p);
         launch_fill(p->em_rf, size_t(p->geo.n_theta) * p->geo.N, 1.f, st);
         backproject_chunk(p, p->em_rf, p->em_bp, 1, st);
         check_launch("sensitivity");
@@ -916,8 +869,9 @@ int lpr_gpu_em(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, in
         if (batch < 0 || iters < 0 || (batch > 0 && (!d_sino || !d_img)))
             throw std::invalid_argument("em: bad buffers, batch or iters");
         ck(cudaSetDevice(p->device), "cudaSetDevice");
-        em_buffers(p);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const Call call(p, st);
+        em_buffers(p);
         const lpr_geometry& G = p->geo;
         const size_t ps = size_t(G.n_theta) * G.N, pi = size_t(G.N) * G.N;
         double* ll = nullptr;
@@ -963,6 +917,7 @@ int lpr_gpu_em_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batc
         }
         int rc = LPR_OK;
         cudaStream_t st = p->stream;
+        const Call call(p, st);
         try {
             ck(cudaMemcpyAsync(dg, h_sino, sizeof(float) * ps * batch, cudaMemcpyHostToDevice, st), "H2D");
             if (!init) ck(cudaMemcpyAsync(df, h_img, sizeof(float) * pi * batch, cudaMemcpyHostToDevice, st), "H2D");
@@ -985,14 +940,14 @@ int lpr_gpu_em_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batc
 int lpr_gpu_radon(lpr_gpu_plan* p, const float* d_img, float* d_sino, int batch, void* stream) {
     return guard([&] {
         run_device(p, radon_chunk, d_img, d_sino, batch, size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0),
-                   size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0), stream, radon_chunk_s);
+                   size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0), stream);
     });
 }
 
 int lpr_gpu_backproject(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, void* stream) {
     return guard([&] {
         run_device(p, backproject_chunk, d_sino, d_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
-                   size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream, backproject_chunk_s);
+                   size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream);
     });
 }
 
@@ -1051,7 +1006,6 @@ int lpr_gpu_radon_transpose_host(lpr_gpu_plan* p, const float* h_sino, float* h_
 
 int lpr_gpu_radon_transpose(lpr_gpu_plan* p, const float* d_sino, float* d_img, int batch, void* stream) {
     return guard([&] {
-        if (p && p->tex_gather) throw std::invalid_argument("radon_transpose: not defined for a texture-gather plan");
         run_device(p, transpose_chunk, d_sino, d_img, batch, size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0),
                    size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0), stream);
     });
@@ -1069,6 +1023,7 @@ int lpr_gpu_profile_stages(lpr_gpu_plan* p, int op, const float* d_in, float* d_
         for (auto& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
         std::vector<double> acc(ns, 0.0);
         cudaStream_t st = p->stream;
+        const Call call(p, st);
         for (int r = 0; r < reps; ++r) {
             p->prof = ev.data();
             try {

@@ -58,13 +58,7 @@ __device__ __forceinline__ void bsw2(float2 a, float2 w[4]) {
 }  // namespace
 
 // ------------------------------------------------------------- prefilter
-// The cubic B-spline prefilter (bspline.cpp:83-130: causal + anticausal IIR
-// with pole z = sqrt(3) - 2, mirror extension) has the two-sided impulse
-// response h_d = sqrt(3) z^|d|. Truncated at |d| <= 16 (|z|^17 ~ 2e-10) it
-// is a 33-tap separable FIR on the mirror-extended line: every output is
-// independent, so lines need no sequential scan and both passes coalesce.
-
-// Recursive form of the same prefilter, for the R path: a 64 x 64 output
+// The cubic B-spline prefilter (bspline.cpp:83-130), recursive: a 64 x 64 output
 // tile is staged with a 16-sample warm-up margin per side (through the
 // mirror map), then each thread runs the causal + anticausal recursion
 // (pole z = sqrt(3) - 2, bspline.cpp:93-106) along one row, then along one
@@ -598,7 +592,7 @@ __device__ __forceinline__ float gather_tex(const DevGeom& g, const FineRow& r, 
     const float gc0 = wc[0] + wc[1], gc1 = wc[2] + wc[3], gr0 = wr[0] + wr[1], gr1 = wr[2] + wr[3];
     const float x0 = kc + float(kApron - 1) + __fdividef(wc[1], gc0) + 0.5f;
     const float x1 = kc + float(kApron + 1) + __fdividef(wc[3], gc1) + 0.5f;
-    const float yb = float((b + g.sb0) * g.pitch) + kr + 0.5f;
+    const float yb = float(b * g.pitch) + kr + 0.5f;
     const float y0 = yb + float(kApron - 1) + __fdividef(wr[1], gr0);
     const float y1 = yb + float(kApron + 1) + __fdividef(wr[3], gr1);
     const float top = fmaf(gc0, tex2D<float>(g.qtex, x0, y0), gc1 * tex2D<float>(g.qtex, x1, y0));
@@ -848,7 +842,7 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
     const int m = blockIdx.y, b = blockIdx.z;
     const int l0b = 2 * P * blockIdx.x;
     const int nts = NTS ? NTS : g.nts, L2 = 2 * nts, n = NR ? NR : g.n_rho;
-    const int lps = NR ? (NR + 6) / 4 * 4 : g.lps;
+    const int lps = NR ? lp_stride(NR) : g.lps;
     const int win = NTS ? NTS + 8 : g.win, j0 = NTS ? -NTS / 2 - 4 : g.j0;
     const size_t item = size_t(b) * g.M + m;
     if (threadIdx.x < P) sms(threadIdx.x)[F::idx(nts)] = make_float2(0.f, 0.f);  // zeroed band edge
@@ -902,46 +896,6 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
             dst[n] = z.x;
             if (l + 1 < 3) dst[n + 1] = z.y;
         }
-    }
-}
-
-// S_m resampling to the sinogram (Alg. 1 step 7). Theta residuals land on
-// lattice rows (sector centres are polar rows), so each sinogram row needs
-// one coefficient row and a 1-D periodic spline along rho; the theta-axis
-// spline weights (1/6, 2/3, 1/6) cancel the theta part of 1/Bhat, which the
-// multiplier therefore omits.
-__global__ void k_radon_out(DevGeom g, const float* __restrict__ lp, float* __restrict__ sino) {
-    extern __shared__ float srow[];
-    const int i = blockIdx.x, b = blockIdx.y;
-    const int nts = g.nts, n = g.n_rho, N = g.N;
-    const int k = (2 * i + nts) / (2 * nts);
-    const int m = k % g.M;
-    const bool flip = ((k - m) / g.M) & 1;
-    const int j = i - k * nts;
-    const float* src = lp + ((size_t(b) * g.M + m) * g.win + (j - g.j0)) * g.lps;
-    for (int l = threadIdx.x; l < g.lps / 4; l += blockDim.x)  // rows are 16-byte aligned (lps % 4 == 0)
-        reinterpret_cast<float4*>(srow)[l] = __ldg(reinterpret_cast<const float4*>(src) + l);
-    __syncthreads();
-    const float cth = __ldg(g.coarse_cos + j + nts / 2) * g.one_m_aR;
-    const float sgn = flip ? -1.f : 1.f;
-    const float invN = 1.f / float(N);
-    float* out = sino + (size_t(b) * g.n_theta + i) * N;
-    for (int c = threadIdx.x; c < N; c += blockDim.x) {
-        const float sp = sgn * float(2 * c - N) * invN;  // (x / N exactly for power-of-two N)
-        const float rho = logf(fmaf(g.aR, sp, cth));
-        const float t = (rho - g.log_ar) * g.inv_drho;
-        const float kf = floorf(t);
-        float w[4];
-        bsw(t - kf, w);
-        const int k0 = int(kf) - 1;
-        float acc = 0.f;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            int idx = k0 + a;
-            idx = idx < 0 ? idx + n : (idx >= n ? idx - n : idx);
-            acc = fmaf(w[a], srow[idx], acc);
-        }
-        out[c] = acc * g.out_scale;
     }
 }
 
@@ -1188,7 +1142,7 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
         float sacc = 0.f;
         if (g.lptex) {  // four tld4 gathers (2 x 2 texels each, exact fp32)
             const float x0 = float(c0 + 1), x1 = x0 + 2.f;
-            const float y0 = float(((b + g.sb0) * g.M + m) * g.win + int(kt) - 1 - g.j0) + 1.f, y1 = y0 + 2.f;
+            const float y0 = float((b * g.M + m) * g.win + int(kt) - 1 - g.j0) + 1.f, y1 = y0 + 2.f;
             const float4 a = tex2Dgather<float4>(g.lptex, x0, y0, 0), e = tex2Dgather<float4>(g.lptex, x1, y0, 0);
             const float4 d = tex2Dgather<float4>(g.lptex, x0, y1, 0), f = tex2Dgather<float4>(g.lptex, x1, y1, 0);
             const float r0 = fmaf(wr[0], a.w, fmaf(wr[1], a.z, fmaf(wr[2], e.w, wr[3] * e.z)));
@@ -1223,9 +1177,13 @@ __global__ void k_bp_out(DevGeom g, const float* __restrict__ lp, float* __restr
     *out = 2.f * acc;
 }
 
-// k_radon_out with SB slices per block: the SB lattice rows are staged
-// together and each sinogram bin's rho coordinate (logf) and spline weights
-// are computed once for all of them.
+// S_m resampling to the sinogram (Alg. 1 step 7). Theta residuals land on
+// lattice rows (sector centres are polar rows), so each sinogram row needs
+// one coefficient row and a 1-D periodic spline along rho; the theta-axis
+// spline weights (1/6, 2/3, 1/6) cancel the theta part of 1/Bhat, which the
+// multiplier therefore omits. SB slices per block: the SB lattice rows are
+// staged together and each sinogram bin's rho coordinate (logf) and spline
+// weights are computed once for all of them.
 template <int SB>
 __global__ void __launch_bounds__(256) k_radon_out_b(DevGeom g, const float* __restrict__ lp, float* __restrict__ sino,
                                                      int nb) {
@@ -1274,28 +1232,16 @@ __global__ void __launch_bounds__(256) k_radon_out_b(DevGeom g, const float* __r
 
 // ------------------------------------------------------------- host launchers
 // R output resampling: SB = kOutSlices slices per block (k_radon_out_b,
-// 0.434 -> 0.373 ms / 16 slices); LPR_OUT_BATCH=0 selects the one-slice kernel (A/B).
+// 0.434 -> 0.373 ms / 16 slices against one slice per block).
 // (The same for k_bp_out, SB slices per thread sharing the atan/log
 // coordinates, measured 1.107 -> 1.104: that kernel is bound by its tld4 gathers.)
-static bool out_batched() {
-    static const bool on = [] {
-        const char* e = std::getenv("LPR_OUT_BATCH");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
 cudaError_t prepare_out_kernels(int lps) {
-    cudaError_t e = cudaFuncSetAttribute(k_radon_out, cudaFuncAttributeMaxDynamicSharedMemorySize, lps * int(sizeof(float)));
-    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_radon_out_b<kOutSlices>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kOutSlices * lps * int(sizeof(float)));
 }
 void launch_radon_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* sino) {
-    if (out_batched())
-        k_radon_out_b<kOutSlices><<<dim3(g.n_theta, (nb + kOutSlices - 1) / kOutSlices), 256,
-                                    size_t(kOutSlices) * g.lps * sizeof(float), st>>>(g, lp, sino, nb);
-    else
-        k_radon_out<<<dim3(g.n_theta, nb), 256, g.lps * sizeof(float), st>>>(g, lp, sino);
+    k_radon_out_b<kOutSlices><<<dim3(g.n_theta, (nb + kOutSlices - 1) / kOutSlices), 256,
+                                size_t(kOutSlices) * g.lps * sizeof(float), st>>>(g, lp, sino, nb);
 }
 void launch_bp_out(int nb, cudaStream_t st, const DevGeom& g, const float* lp, float* img) {
     // (the sector loop unrolled for M = 3, all 12 tld4 gathers in flight: 1.107 -> 1.106)
@@ -1405,12 +1351,8 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
         return;
     }
 #define CALL(F) k_radon_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qf, qft, spec)
-    static const bool band = [] {  // LPR_FINE_BAND=0: the unpruned plans (A/B)
-        const char* e = std::getenv("LPR_FINE_BAND");
-        return !(e && e[0] == '0');
-    }();
     if (L.variant == kFft8192) {
-        if (g.pitch == kPitch2048 && band && g.Lf == 8 * g.nts && g.nts == 1024)
+        if (g.pitch == kPitch2048 && g.Lf == 8 * g.nts && g.nts == 1024)
             k_radon_theta_fwd<Fft8192Band, 0, kPitch2048, 1024><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(
                 g, fd, qf, qft, spec);
         else if (g.pitch == kPitch2048)
@@ -1420,7 +1362,7 @@ void launch_radon_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, cons
             CALL(Fft8192Band);
         return;
     }
-    if (L.variant == kFft16384 && band && g.Lf == 8 * g.nts && g.nts == 2048) {  // N = 4096: band-pruned, radix 2 fused into the store
+    if (L.variant == kFft16384 && g.Lf == 8 * g.nts && g.nts == 2048) {  // N = 4096: band-pruned, radix 2 fused into the store
         k_radon_theta_fwd<Fft16384Band, 0, 0, 2048><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(
             g, fd, qf, qft, spec);
         return;
@@ -1458,7 +1400,7 @@ void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGe
 
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                       const float2* spec, float* lp) {
-    if (L.variant == kFft2048 && g.n_rho == kNRho2048 && g.nts == 1024 && g.lps == (kNRho2048 + 6) / 4 * 4 &&
+    if (L.variant == kFft2048 && g.n_rho == kNRho2048 && g.nts == 1024 && g.lps == lp_stride(kNRho2048) &&
         g.win == 1024 + 8 && g.j0 == -512 - 4) {
         k_theta_inv<Fft2048, kNRho2048, 1024><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, spec, lp);
         return;

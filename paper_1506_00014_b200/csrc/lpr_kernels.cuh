@@ -20,6 +20,12 @@ constexpr int kApron = 4;     // mirrored border around the image coefficients
 constexpr int kFirHalf = 16;  // B-spline prefilter impulse-response half length
 constexpr int kOutSlices = 4;  // slices per block of the R output resampling kernel
 
+// Row stride of the theta-inverse window buffer lp: n_rho columns + 3
+// periodic copies (rho taps never wrap), rounded up to 8 floats (32-byte rows,
+// the texture pitch of k_bp_out's tld4 view). One definition for the plan and
+// the kernels specialised on a compile-time N_rho.
+__host__ __device__ constexpr int lp_stride(int n_rho) { return (n_rho + 3 + 7) / 8 * 8; }
+
 // Everything a kernel needs about the plan, passed by value.
 struct DevGeom {
     int N, M, n_theta, nts, n_rho, refine;
@@ -44,7 +50,6 @@ struct DevGeom {
     const float* fir;         // 2 kFirHalf + 1 prefilter taps
     cudaTextureObject_t qtex; // texture-gather ablation: coefficient raster (0 unless enabled)
     cudaTextureObject_t lptex; // tld4 view of lp for k_bp_out (0 unless enabled)
-    int sb0;                   // first scratch slice of this launch (the textures span the whole scratch)
 };
 
 // FFT kernel variants: a compile-time register FFT for the hot lengths

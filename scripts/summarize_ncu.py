@@ -5,10 +5,12 @@ files under profiles/<tag>/:
                         `--metrics gpu__time_duration.sum` pass)
   ncu_full_summary.md   key `--set full` metrics per kernel (time, DRAM bytes,
                         L1/shared wavefronts, bank conflicts, occupancy, issue)
-  ncu_dram_bytes.json   per-launch DRAM traffic of each kernel, per slice,
-                        read by bench.py for the roofline "traffic" field
+  ncu_kernels.json      per kernel: the batch of the captured launch, its
+                        DRAM traffic (dram__bytes_read + write) and L1/LSU
+                        utilisation; read by bench.py for the roofline
+                        "traffic" field (scaled to the bench batch)
 
-    python scripts/summarize_ncu.py gpurun_out profiles/round1 [slices_per_launch]
+    python scripts/summarize_ncu.py gpurun_out profiles/round2 [slices_per_launch]
 """
 import csv
 import json
@@ -43,7 +45,7 @@ def short_name(k):
 
 def main():
     src, dst = sys.argv[1], sys.argv[2]
-    slices = float(sys.argv[3]) if len(sys.argv) > 3 else 2.0
+    slices = float(sys.argv[3]) if len(sys.argv) > 3 else 16.0
     os.makedirs(dst, exist_ok=True)
     if os.path.exists(os.path.join(src, "launches.csv")):
         shutil.copy(os.path.join(src, "launches.csv"), os.path.join(dst, "launches.csv"))
@@ -73,16 +75,18 @@ def main():
             scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}
             rd *= scale.get(units[hdr.index("dram__bytes_read.sum")], 1.0)
             wr *= scale.get(units[hdr.index("dram__bytes_write.sum")], 1.0)
-            traffic[name] = (rd + wr) / slices
+            traffic[name] = rd + wr
             key = "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed"
             if key in hdr:
                 lsu[name] = float(d[hdr.index(key)])
     with open(os.path.join(dst, "ncu_full_summary.md"), "w") as f:
-        f.write(f"ncu --set full, {os.path.basename(rep)}; one R and one R# on {slices:g} slices at N=2048 "
-                "(scripts/profile_one.py), cold-cache replays.\n\n")
+        f.write(f"ncu --set full --clock-control none, {os.path.basename(rep)}; one R and one R# launch of "
+                f"{slices:g} slices at N=2048 (the bench plan and batch; scripts/profile_one.py), cache "
+                "flushed between replays.\n\n")
         f.write("\n".join(lines) + "\n")
-    with open(os.path.join(dst, "ncu_dram_bytes.json"), "w") as f:
-        json.dump({"per_slice_bytes": traffic, "lsu_wavefronts_pct": lsu, "slices_per_launch": slices}, f, indent=1)
+    with open(os.path.join(dst, "ncu_kernels.json"), "w") as f:
+        json.dump({"source": os.path.basename(rep), "kernels": {
+            n: {"batch": slices, "dram_bytes": traffic[n], "lsu_pct": lsu.get(n)} for n in traffic}}, f, indent=1)
 
 
 if __name__ == "__main__":
