@@ -508,7 +508,6 @@ __device__ __forceinline__ bool fine_pos(const DevGeom& g, const FineRow& r, flo
 // 32 consecutive samples again walk along raster rows.
 constexpr int kPitch2048 = 2048 + 2 * kApron;  // raster pitch of the N = 2048 plans (the bench size)
 constexpr int kNTheta2048 = 3072;              // their angle count (the Qg^T row stride)
-constexpr int kNRho2048 = 4374;                // and their (7-smooth) N_rho
 
 // SCALE = false leaves out the e^rho factor (constant along a column: the
 // fused kernel applies it to the column's spectrum instead of every sample).
@@ -829,9 +828,9 @@ cudaError_t prepare_rho_pad() {
 
 // Hermitian theta inverse: two real columns per complex transform of length
 // 2 nts; rows [j0, j0 + win) of the periodic result are kept.
-// NR, NTS > 0: N_rho and nts at compile time (the N = 2048 bench plan: 4374,
-// 1024), so row strides and the window geometry become immediates.
-template <class F, int NR = 0, int NTS = 0>
+// (A variant with N_rho = 4374 and nts = 1024 at compile time measured slower:
+// 0.780 -> 0.943 ms per 16 slices.)
+template <class F>
 __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                       const float2* __restrict__ spec, float* __restrict__ lp) {
     extern __shared__ float2 smem[];
@@ -841,9 +840,9 @@ __global__ void LPR_LB(F) k_theta_inv(const __grid_constant__ DevGeom g, const _
     const Slots sms{smem, E};
     const int m = blockIdx.y, b = blockIdx.z;
     const int l0b = 2 * P * blockIdx.x;
-    const int nts = NTS ? NTS : g.nts, L2 = 2 * nts, n = NR ? NR : g.n_rho;
-    const int lps = NR ? lp_stride(NR) : g.lps;
-    const int win = NTS ? NTS + 8 : g.win, j0 = NTS ? -NTS / 2 - 4 : g.j0;
+    const int nts = g.nts, L2 = 2 * nts, n = g.n_rho;
+    const int lps = g.lps;
+    const int win = g.win, j0 = g.j0;
     const size_t item = size_t(b) * g.M + m;
     if (threadIdx.x < P) sms(threadIdx.x)[F::idx(nts)] = make_float2(0.f, 0.f);  // zeroed band edge
     load_packed_hermitian<F>(sms, spec + item * size_t(nts + 1) * n, nts, L2, n, l0b);
@@ -1328,7 +1327,6 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
     if (rho.variant == kFft4374) SET(k_rho_stream<Rho4374>, rho_stream_smem(kFft4374));
 #define COARSE(F)                                          \
     SET(k_theta_inv<F>, coarse.smem * coarse.per_block);    \
-    SET((k_theta_inv<F, kNRho2048, 1024>), coarse.smem * coarse.per_block); \
     SET(k_bp_theta_fwd<F>, coarse.smem * coarse.per_block); \
     SET((k_bp_theta_fwd<F, kNTheta2048>), coarse.smem * coarse.per_block); \
     SET(k_theta_fwd_T<F>, coarse.smem * coarse.per_block)
@@ -1400,11 +1398,6 @@ void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGe
 
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                       const float2* spec, float* lp) {
-    if (L.variant == kFft2048 && g.n_rho == kNRho2048 && g.nts == 1024 && g.lps == lp_stride(kNRho2048) &&
-        g.win == 1024 + 8 && g.j0 == -512 - 4) {
-        k_theta_inv<Fft2048, kNRho2048, 1024><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, spec, lp);
-        return;
-    }
 #define CALL(F) k_theta_inv<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, spec, lp)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL

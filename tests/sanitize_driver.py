@@ -1,10 +1,11 @@
 """Driver for compute-sanitizer (tests/test_sanitizer.py): every kernel of R,
 R#, R^T, the FBP filter and one EM step at N=64 through the host-buffer C ABI
-(numpy only, no torch), both plan kinds (default N_rho, 7-smooth N_rho)."""
+(numpy buffers; torch only for the device-resident EM entry point), both plan kinds (default N_rho, 7-smooth N_rho)."""
 import os
 import sys
 
 import numpy as np
+import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1506_00014_b200 as lp  # noqa: E402
@@ -19,7 +20,8 @@ for n_rho in (0, lp.smooth_n_rho(N)):
     b = lp.fast_backprojection(s, plan)
     t = lp.radon_transpose(s, plan)
     fb = lp.fbp(s, plan, "ramp")
-    em, _ = lp.em_run(np.abs(s[0]), plan, 1)
+    em, _ = lp.em_run(torch.tensor(np.abs(s[0]), device="cuda:0"), plan, 1)
+    em = em.cpu().numpy()
     assert np.isfinite(b).all() and np.isfinite(t).all() and np.isfinite(fb).all() and np.isfinite(em).all()
     plan.close()
 print("sanitize driver ok")
