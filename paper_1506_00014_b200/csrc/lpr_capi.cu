@@ -218,8 +218,9 @@ struct lpr_gpu_plan {
             d.twp_inv = upload(rho_stream_inv_twiddles(launch.variant));
             launch.rho_stream = 1;
         }
-        if (launch.smem * launch.per_block > 227 * 1024 ||
-            (staged_row && launch.smem + size_t(n) * sizeof(float2) > 227 * 1024))
+        const bool padded = staged_row && launch.variant == kFftGeneric && rho_pad_length(int(n)) > 0;  // k_rho_pad
+        if (!padded && (launch.smem * launch.per_block > 227 * 1024 ||
+                        (staged_row && launch.smem + size_t(n) * sizeof(float2) > 227 * 1024)))
             throw std::invalid_argument("fft: a length-" + std::to_string(n) + " transform does not fit in shared memory (for a non-7-smooth n_rho this large, use the 7-smooth plan: lpr_smooth_n_rho)");
     }
 
@@ -476,8 +477,15 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     }
 
     ck(prepare_filter_kernel(p->l_filt), "filter smem attribute");
-    ck(prepare_fft_kernels(p->l_fine, p->l_rho, p->l_coarse, size_t(G.n_rho) * sizeof(float2)),
-       "fft smem attributes");
+    {
+        // a plan whose rho pass runs in k_rho_pad never launches the generic rho kernel
+        // (whose Bluestein buffer would not fit, e.g. N_rho = 8666)
+        FftLaunch lr = p->l_rho;
+        const bool padded = p->rho_pad || p->rho_direct;
+        if (padded) lr.smem = 0;
+        ck(prepare_fft_kernels(p->l_fine, lr, p->l_coarse, padded ? 0 : size_t(G.n_rho) * sizeof(float2)),
+           "fft smem attributes");
+    }
     if (p->tex_mode) {
         // the plain coefficient rasters of the whole batch as one tall pitched
         // 2-D texture with hardware bilinear filtering
@@ -535,11 +543,11 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
 void rho_chunk(lpr_gpu_plan* p, int which, int nb, cudaStream_t st, const DevGeom& g, float2* spec) {
     const dim3 grid(g.nts + 1, nb * g.M);
     if (p->rho_pad) {
-        launch_rho_pad(grid, st, g, which == 0 ? p->pad_R : which == 1 ? p->pad_B : p->pad_RT, spec);
+        launch_rho_pad(p->rho_pad, grid, st, g, which == 0 ? p->pad_R : which == 1 ? p->pad_B : p->pad_RT, spec);
         return;
     }
     if (p->rho_direct) {
-        launch_rho_pad(grid, st, g, which == 0 ? p->mult_R : which == 1 ? p->mult_B : p->mult_RT, spec);
+        launch_rho_pad(int(rho_direct_length()), grid, st, g, which == 0 ? p->mult_R : which == 1 ? p->mult_B : p->mult_RT, spec);
         return;
     }
     launch_rho_pass(p->l_rho, grid, st, g, p->d_rho, which == 0 ? p->mult_R : which == 1 ? p->mult_B : p->mult_RT, spec);

@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(F::kT, 2) k_rho_stream(const __grid_constant__
 // GPU in fp64, rho_pad_multipliers). One row per block, the multiplier read
 // from L2 inside the fused middle butterfly; replaces Bluestein (15x slower).
 template <class F>
-__global__ void __launch_bounds__(F::kT, 2) k_rho_pad(const __grid_constant__ DevGeom g,
+__global__ void __launch_bounds__(F::kT, F::kT >= 1024 ? 1 : 2) k_rho_pad(const __grid_constant__ DevGeom g,
                                                       const float2* __restrict__ mult_pad, float2* __restrict__ spec) {
     extern __shared__ __align__(16) float2 sm[];
     const int k = blockIdx.x, item = blockIdx.y, n = g.n_rho, tid = threadIdx.x;
@@ -815,15 +815,28 @@ __global__ void __launch_bounds__(F::kT, 2) k_rho_pad(const __grid_constant__ De
 
 size_t rho_direct_length() { return RhoPad8748::kN; }
 
-size_t rho_pad_length(int n_rho) { return (2 * n_rho - 1 <= RhoPad8748::kN && n_rho > 4096) ? RhoPad8748::kN : 0; }
+// padded length for a non-smooth n_rho: 8748 for the N = 2048 default plan
+// (4333), 17496 for N = 4096 (8666); 0: none (Bluestein)
+size_t rho_pad_length(int n_rho) {
+    if (2 * n_rho - 1 <= RhoPad8748::kN && n_rho > 4096) return RhoPad8748::kN;
+    if (2 * n_rho - 1 <= RhoPad17496::kN && n_rho > 8192 && n_rho != RhoPad8748::kN) return RhoPad17496::kN;  // 8748: direct
+    return 0;
+}
 
-void launch_rho_pad(dim3 grid, cudaStream_t st, const DevGeom& g, const float2* mult_pad, float2* spec) {
-    k_rho_pad<RhoPad8748><<<grid, RhoPad8748::kT, sizeof(float2) * RhoPad8748::kElems, st>>>(g, mult_pad, spec);
+void launch_rho_pad(int nb, dim3 grid, cudaStream_t st, const DevGeom& g, const float2* mult_pad, float2* spec) {
+    if (nb == RhoPad17496::kN)
+        k_rho_pad<RhoPad17496><<<grid, RhoPad17496::kT, sizeof(float2) * RhoPad17496::kElems, st>>>(g, mult_pad, spec);
+    else
+        k_rho_pad<RhoPad8748><<<grid, RhoPad8748::kT, sizeof(float2) * RhoPad8748::kElems, st>>>(g, mult_pad, spec);
 }
 
 cudaError_t prepare_rho_pad() {
-    return cudaFuncSetAttribute((const void*)k_rho_pad<RhoPad8748>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(sizeof(float2) * RhoPad8748::kElems));
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_rho_pad<RhoPad8748>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sizeof(float2) * RhoPad8748::kElems));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute((const void*)k_rho_pad<RhoPad17496>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(float2) * RhoPad17496::kElems));
 }
 
 // Hermitian theta inverse: two real columns per complex transform of length

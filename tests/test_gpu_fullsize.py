@@ -73,14 +73,18 @@ def test_exact_transpose_identity_n2048(lp, lpo, cuda):
         assert abs(a - b) <= 1e-5 * abs(a) and gap <= 1e-5, (i, a, b, gap)
 
 
-def test_config5_n4096_against_oracle(lp, lpo, cuda):
-    """Config 5 (N=4096, 6144 angles, 7-smooth N_rho=8748): one slice each
-    way against the oracle."""
+@pytest.mark.parametrize("smooth", [True, False])
+def test_config5_n4096_against_oracle(lp, lpo, cuda, smooth):
+    """Config 5 (N=4096, 6144 angles): one slice each way against the oracle,
+    on the 7-smooth plan (N_rho=8748) and on the reference's own
+    sampling_plan(4096, 3) (N_rho=8666 = 2 * 7 * 619, whose rho convolution
+    runs zero-padded over 17496 = 2^3 3^7, geometry.cpp:85-88)."""
     import torch
 
     N = 4096
-    n_rho = lp.smooth_n_rho(N)
+    n_rho = lp.smooth_n_rho(N) if smooth else 0
     g = lp.sampling_plan(N, 3, 0, n_rho)
+    assert g.n_rho == (8748 if smooth else 8666)
     p = lpo.make_plan(N, 3, 0, n_rho)
     z, zb = lpo.spectrum(p, 0), lpo.spectrum(p, 1)
     plan = lp.RadonPlan(g, z, zb, max_batch=1)
@@ -91,7 +95,7 @@ def test_config5_n4096_against_oracle(lp, lpo, cuda):
     wantb = lpo.fast_backprojection(p, zb, got.astype(np.float64))
     gotb = lp.fast_backprojection(torch.tensor(got, device=cuda), plan).cpu().numpy()
     eb = lpo.rel_l2(gotb, wantb)
-    print(f"N=4096 n_rho={n_rho}: R rel_l2 {er:.3e}, R# rel_l2 {eb:.3e}")
+    print(f"N=4096 n_rho={g.n_rho}: R rel_l2 {er:.3e}, R# rel_l2 {eb:.3e}")
     assert er <= TOL and eb <= TOL, (er, eb)
 
 
