@@ -72,6 +72,17 @@ int lpr_spectrum_quadrature(const lpr_geometry* geom, int kind, double* out_re_i
  * written to the host array out_re_im. Plans created with NULL spectra use it. */
 int lpr_gpu_spectrum_quadrature(int device, const lpr_geometry* geom, int kind, double* out_re_im);
 
+/* On-disk spectrum cache keyed by (kind, N, M, n_theta, n_rho):
+ * lpr_spectrum_quadrature, lpr_gpu_spectrum_quadrature and plan creation with
+ * NULL spectra read a cached spectrum (full fp64) instead of recomputing it,
+ * and store what they compute. dir = NULL disables the cache; until this is
+ * called the directory comes from the environment variable
+ * LPR_SPECTRUM_CACHE (unset: disabled). The counters report cache reads and
+ * writes since the library was loaded. */
+int lpr_spectrum_cache_dir(const char* dir);
+long long lpr_spectrum_cache_hits(void);
+long long lpr_spectrum_cache_stores(void);
+
 /* Device plan: uploads the spectra (folded with 1/Bhat and the FFT
  * normalisation, fp32) and allocates scratch for max_batch slices. Either
  * spectrum may be NULL, in which case it is computed here. */

@@ -18,6 +18,8 @@ from .lp_ops import (  # noqa: F401
     radon_transpose,
     sampling_plan,
     sensitivity_image,
+    set_spectrum_cache,
+    spectrum_cache_counters,
     smooth_n_rho,
     zeta_bp_spectrum,
     zeta_spectrum,

@@ -57,6 +57,9 @@ EXPORTS = {
     "lpr_gpu_fft_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_last_error": (ctypes.c_char_p, []),
     "lpr_gpu_spectrum_quadrature": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+    "lpr_spectrum_cache_dir": (ctypes.c_int, [ctypes.c_char_p]),
+    "lpr_spectrum_cache_hits": (ctypes.c_longlong, []),
+    "lpr_spectrum_cache_stores": (ctypes.c_longlong, []),
     "lpr_gpu_sensitivity": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "lpr_gpu_sensitivity_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "lpr_gpu_em": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,

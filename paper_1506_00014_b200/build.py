@@ -28,7 +28,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-Xpt
               "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 
 CU_SOURCES = ["lpr_kernels.cu", "lpr_transpose.cu", "lpr_capi.cu", "lpr_spectrum.cu", "lpr_em.cu"]
-CXX_SOURCES = ["lpr_host.cpp"]
+CXX_SOURCES = ["lpr_host.cpp", "lpr_cache.cpp"]
 
 
 def _nvcc() -> str:

@@ -323,16 +323,16 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     // spectral multipliers on the half theta spectrum k in [0, nts]
     const long nts = G.nts, nr = G.n_rho, rows = 2 * nts;
     std::vector<double> zbuf, zbbuf;
-    if (!zeta) {
-        zbuf.resize(2 * rows * nr);
-        spectrum_gpu(p->device, G, 0, zbuf.data());
-        zeta = zbuf.data();
-    }
-    if (!zeta_bp) {
-        zbbuf.resize(2 * rows * nr);
-        spectrum_gpu(p->device, G, 1, zbbuf.data());
-        zeta_bp = zbbuf.data();
-    }
+    auto computed = [&](int kind, std::vector<double>& buf) {  // on-disk cache, else the GPU quadrature
+        buf.resize(2 * rows * nr);
+        if (!host::spectrum_cache_load(G, kind, buf.data())) {
+            spectrum_gpu(p->device, G, kind, buf.data());
+            host::spectrum_cache_store(G, kind, buf.data());
+        }
+        return buf.data();
+    };
+    if (!zeta) zeta = computed(0, zbuf);
+    if (!zeta_bp) zeta_bp = computed(1, zbbuf);
     auto bhat = [](long k, long n) { return (2.0 + std::cos(2.0 * kPi * double(k) / double(n))) / 3.0; };
     std::vector<float2> mr((nts + 1) * nr), mb((nts + 1) * nr);
     const double sr = 1.0 / (double(g.Lf) * double(nr)), sb = 1.0 / (double(rows) * double(nr));
@@ -796,7 +796,10 @@ int lpr_smooth_n_rho(int N, int M) {
 int lpr_spectrum_quadrature(const lpr_geometry* geom, int kind, double* out) {
     return guard([&] {
         if (!geom || !out || (kind != 0 && kind != 1)) throw std::invalid_argument("bad spectrum arguments");
-        host::spectrum(*geom, kind, out);
+        const lpr_geometry G = host::make_geometry(geom->N, geom->M, geom->n_theta, geom->n_rho);
+        if (host::spectrum_cache_load(G, kind, out)) return;
+        host::spectrum(G, kind, out);
+        host::spectrum_cache_store(G, kind, out);
     });
 }
 
@@ -804,9 +807,18 @@ int lpr_gpu_spectrum_quadrature(int device, const lpr_geometry* geom, int kind, 
     return guard([&] {
         if (!geom || !out || (kind != 0 && kind != 1)) throw std::invalid_argument("bad spectrum arguments");
         const lpr_geometry G = host::make_geometry(geom->N, geom->M, geom->n_theta, geom->n_rho);
+        if (host::spectrum_cache_load(G, kind, out)) return;
         spectrum_gpu(device, G, kind, out);
+        host::spectrum_cache_store(G, kind, out);
     });
 }
+
+int lpr_spectrum_cache_dir(const char* dir) {
+    return guard([&] { host::set_spectrum_cache_dir(dir); });
+}
+
+long long lpr_spectrum_cache_hits(void) { return host::spectrum_cache_hits(); }
+long long lpr_spectrum_cache_stores(void) { return host::spectrum_cache_stores(); }
 
 int lpr_gpu_plan_create(int device, const lpr_geometry* geom, const double* zeta, const double* zeta_bp,
                         int max_batch, lpr_gpu_plan** out) {

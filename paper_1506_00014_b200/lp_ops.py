@@ -20,6 +20,7 @@ entry points (H2D, compute, D2H inside the call).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -47,6 +48,17 @@ def _spectrum(g: Geometry, kind: int, device) -> np.ndarray:
     else:
         check(lib().lpr_gpu_spectrum_quadrature(int(device), ctypes.byref(g), kind, out.ctypes.data))
     return out
+
+
+def set_spectrum_cache(directory) -> None:
+    """Directory of the on-disk spectrum cache keyed by (kind, N, M, n_theta,
+    n_rho); None disables it. Default: $LPR_SPECTRUM_CACHE."""
+    check(lib().lpr_spectrum_cache_dir(None if directory is None else os.fsencode(directory)))
+
+
+def spectrum_cache_counters() -> tuple:
+    """(reads served from the cache, spectra written to it) since load."""
+    return int(lib().lpr_spectrum_cache_hits()), int(lib().lpr_spectrum_cache_stores())
 
 
 def zeta_spectrum(g: Geometry, device=None) -> np.ndarray:
