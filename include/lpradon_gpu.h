@@ -145,6 +145,11 @@ int lpr_gpu_radon_transpose_host(lpr_gpu_plan* plan, const float* h_sino, float*
 int lpr_gpu_profile_stages(lpr_gpu_plan* plan, int op, const float* d_in, float* d_out, int batch, int reps,
                            double* ms, int* nstages, const char** names);
 
+/* The same on host input h_in (copied once into the plan's staging buffer
+ * before the timed launches; the outputs stay on the device). */
+int lpr_gpu_profile_stages_host(lpr_gpu_plan* plan, int op, const float* h_in, int batch, int reps, double* ms,
+                                int* nstages, const char** names);
+
 /* Kernel launches issued by this plan since creation (instrumentation). */
 long long lpr_gpu_launch_count(const lpr_gpu_plan* plan);
 /* Spectral-convolution launches (the reference's 2-D FFT counter analogue:

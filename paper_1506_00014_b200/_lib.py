@@ -53,6 +53,9 @@ EXPORTS = {
     "lpr_gpu_fbp": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                    ctypes.c_void_p]),
     "lpr_gpu_fbp_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "lpr_gpu_profile_stages_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                                   ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_char_p)]),
     "lpr_gpu_launch_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_fft_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_last_error": (ctypes.c_char_p, []),

@@ -86,12 +86,30 @@ def build(verbose: bool = False) -> str:
         _run([nvcc, "-ccbin", _host_cxx(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread",
               "-L" + CUDA_LIB, "-lcufft", "-Xlinker", "-rpath=" + CUDA_LIB],
              os.path.join(BUILD, "link.log"))
+    build_cli()
     if verbose:
         for src in CU_SOURCES:
             log = os.path.join(BUILD, src + ".o.log")
             if os.path.exists(log):
                 print(open(log).read())
     return LIB
+
+
+CLI = os.path.join(PKG, "bin", "lpradon")
+
+
+def build_cli() -> str:
+    """The C++ command-line tool (csrc/cli: LPT1 containers + the reference's
+    CLI subcommands over the C ABI), linked against the in-tree library."""
+    if _VARIANT:
+        return CLI
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    srcs = [os.path.join(CSRC, "cli", f) for f in ("lpt1.cpp", "lpradon_cli.cpp")]
+    deps = srcs + [LIB, os.path.join(ROOT, "include", "lpradon", "lpt1.hpp"), os.path.join(ROOT, "include", "lpradon_gpu.h")]
+    if _stale(CLI, deps):
+        _run([_host_cxx(), "-O2", "-std=c++17", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"), *srcs,
+              "-o", CLI, "-L" + PKG, "-llpradon_gpu", "-Wl,-rpath,$ORIGIN/.."], os.path.join(BUILD, "cli.log"))
+    return CLI
 
 
 REF_INCLUDE = "/root/reference/proj/include"

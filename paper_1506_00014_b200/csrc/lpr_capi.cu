@@ -1068,6 +1068,24 @@ int lpr_gpu_profile_stages(lpr_gpu_plan* p, int op, const float* d_in, float* d_
     });
 }
 
+int lpr_gpu_profile_stages_host(lpr_gpu_plan* p, int op, const float* h_in, int batch, int reps, double* ms,
+                                int* nstages, const char** names) {
+    return guard([&] {
+        if (!p || !h_in || batch < 1 || batch > p->max_batch) throw std::invalid_argument("profile: bad arguments");
+        const lpr_geometry& G = p->geo;
+        const size_t n = size_t(batch) * (op == 0 ? size_t(G.N) * G.N : size_t(G.n_theta) * G.N);
+        {
+            const std::lock_guard<std::recursive_mutex> lk(p->mu);
+            ck(cudaSetDevice(p->device), "cudaSetDevice");
+            if (p->has_done) ck(cudaStreamWaitEvent(p->stream, p->ev_done, 0), "cudaStreamWaitEvent");
+            ck(cudaMemcpyAsync(p->d_in, h_in, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "H2D");
+            ck(cudaStreamSynchronize(p->stream), "stream sync");
+        }
+        const int rc = lpr_gpu_profile_stages(p, op, p->d_in, p->d_out, batch, reps, ms, nstages, names);
+        if (rc != LPR_OK) throw Error(lpr_status(rc), g_last_error);
+    });
+}
+
 long long lpr_gpu_launch_count(const lpr_gpu_plan* p) { return p ? p->launches : -1; }
 long long lpr_gpu_fft_count(const lpr_gpu_plan* p) { return p ? p->ffts : -1; }
 
