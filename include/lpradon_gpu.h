@@ -106,6 +106,17 @@ int lpr_gpu_backproject(lpr_gpu_plan* plan, const float* d_sino, float* d_img, i
  * and <f,u>_X = sum(f u) / N^2, so <R f, g>_Sigma = <f, R^T g>_X. */
 int lpr_gpu_radon_transpose(lpr_gpu_plan* plan, const float* d_sino, float* d_img, int batch, void* stream);
 
+/* lp_convolve, the spectral convolution of Alg. 1 step 6 /
+ * Alg. 2 step 4 as a standalone operator: for each of `batch` real rasters on
+ * the doubled grid (2 nts rows in periodic order x n_rho columns, row-major,
+ * device), out = Re IFFT2(FFT2(in) * S [/ (Bhat_theta Bhat_rho)]) with S the
+ * host (2 nts) x n_rho complex fp64 spectrum (re/im interleaved, theta rows in
+ * FFT order, even in k_theta like zeta and zeta#: kernel.cpp:228) and its
+ * theta-Nyquist row treated as zero, as Algorithms 1-2 do. Runs the plan's
+ * own theta / rho / theta-inverse kernels; batch may exceed max_batch. */
+int lpr_gpu_lp_convolve(lpr_gpu_plan* plan, const double* spectrum_re_im, int divide_bspline, const float* d_in,
+                        float* d_out, int batch, void* stream);
+
 /* Filtered back-projection (the main caller of R#):
  * kind 0 = ramp, 1 = Shepp-Logan, 2 = cosine transfer functions along s
  * (discrete band-limited ramp with end-point correction, 2N zero padding).

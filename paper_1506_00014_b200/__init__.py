@@ -15,6 +15,7 @@ from .lp_ops import (  # noqa: F401
     fast_radon,
     inner_image,
     inner_sinogram,
+    lp_convolve,
     radon_transpose,
     sampling_plan,
     sensitivity_image,

@@ -56,6 +56,8 @@ EXPORTS = {
     "lpr_gpu_profile_stages_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                                                    ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                                    ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_char_p)]),
+    "lpr_gpu_lp_convolve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "lpr_gpu_launch_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_fft_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_last_error": (ctypes.c_char_p, []),

@@ -124,6 +124,8 @@ struct lpr_gpu_plan {
     int rho_pad = 0;             // padded rho-convolution length (non-smooth N_rho), 0: none
     bool rho_direct = false;     // N_rho == that compile-time length: same kernel, plain multipliers
     float2 *pad_R = nullptr, *pad_B = nullptr, *pad_RT = nullptr;  // its multipliers, (nts + 1) x rho_pad
+    float2* lpc_mult = nullptr;  // lp_convolve: the call's multipliers ((nts + 1) x (rho_pad or n_rho))
+    float* lpc_out = nullptr;    // lp_convolve: theta-inverse output, max_batch x 2 nts x lps
     float* band = nullptr;       // banded transpose of the apron-extended 1-D prefilter
     int band_h = 0;
     float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
@@ -705,6 +707,32 @@ void run_device(lpr_gpu_plan* p, ChunkFn fn, const float* in, float* out, int ba
     }
 }
 
+// lp_convolve on nb doubled-grid rasters with the
+// multipliers set in p->lpc_mult: theta FFT -> rho pass -> Hermitian theta
+// inverse over all 2 nts rows -> compaction to row stride n_rho.
+void lpc_chunk(lpr_gpu_plan* p, const float* in, float* out, int nb, cudaStream_t st) {
+    DevGeom g = p->g;
+    g.M = 1;  // one item per raster
+    const int nr = g.n_rho, rows = g.L2;
+    launch_lpc_theta_fwd(p->l_coarse, dim3(cdiv(nr, 2), 1, nb), st, g, p->d_coarse, in, p->spec);
+    const dim3 grid(g.nts + 1, nb);
+    if (p->rho_pad)
+        launch_rho_pad(p->rho_pad, grid, st, g, p->lpc_mult, p->spec);
+    else if (p->rho_direct)
+        launch_rho_pad(int(rho_direct_length()), grid, st, g, p->lpc_mult, p->spec);
+    else
+        launch_rho_pass(p->l_rho, grid, st, g, p->d_rho, p->lpc_mult, p->spec);
+    g.win = rows;  // every row of the period, in natural order
+    g.j0 = 0;
+    launch_theta_inv(p->l_coarse, dim3(cdiv(nr, 2), 1, nb), st, g, p->d_coarse, p->spec, p->lpc_out);
+    ck(cudaMemcpy2DAsync(out, size_t(nr) * sizeof(float), p->lpc_out, size_t(g.lps) * sizeof(float),
+                         size_t(nr) * sizeof(float), size_t(rows) * nb, cudaMemcpyDeviceToDevice, st),
+       "lp_convolve compaction");
+    check_launch("lp_convolve launch");
+    p->launches += 3;
+    p->ffts += nb;
+}
+
 bool is_pinned(const void* ptr) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
@@ -1065,6 +1093,45 @@ int lpr_gpu_profile_stages(lpr_gpu_plan* p, int op, const float* d_in, float* d_
         *nstages = ns;
         if (names)
             for (int i = 0; i < ns; ++i) names[i] = op == 0 ? kRadonStages[i] : kBackprojectStages[i];
+    });
+}
+
+int lpr_gpu_lp_convolve(lpr_gpu_plan* p, const double* spectrum, int divide_bspline, const float* d_in, float* d_out,
+                        int batch, void* stream) {
+    return guard([&] {
+        if (!p || !spectrum) throw std::invalid_argument("lp_convolve: null plan or spectrum");
+        const lpr_geometry& G = p->geo;
+        const long nts = G.nts, nr = G.n_rho, rows = 2 * nts;
+        {
+            const std::lock_guard<std::recursive_mutex> lk(p->mu);
+            ck(cudaSetDevice(p->device), "cudaSetDevice");
+            if (p->has_done) ck(cudaEventSynchronize(p->ev_done), "cudaEventSynchronize");  // lpc_mult is free
+            // multipliers on the half theta spectrum: S(k, v) [/ (Bhat(k) Bhat(v))] / (2 nts n_rho),
+            // the theta-Nyquist row zero as in Algorithms 1-2
+            auto bhat = [](long k, long n) { return (2.0 + std::cos(2.0 * kPi * double(k) / double(n))) / 3.0; };
+            std::vector<double> m64(2 * (nts + 1) * nr, 0.0);
+            const double sc = 1.0 / (double(rows) * double(nr));
+            for (long k = 0; k < nts; ++k)
+                for (long v = 0; v < nr; ++v) {
+                    const double d = divide_bspline ? sc / (bhat(k, rows) * bhat(v, nr)) : sc;
+                    m64[2 * (k * nr + v)] = spectrum[2 * (k * nr + v)] * d;
+                    m64[2 * (k * nr + v) + 1] = spectrum[2 * (k * nr + v) + 1] * d;
+                }
+            const long cols = p->rho_pad ? p->rho_pad : nr;
+            if (!p->lpc_mult) {
+                p->lpc_mult = p->dalloc<float2>(size_t(nts + 1) * cols);
+                p->lpc_out = p->dalloc<float>(size_t(p->max_batch) * rows * p->g.lps);
+            }
+            if (p->rho_pad) {
+                rho_pad_multipliers(p->device, int(nts + 1), int(nr), int(p->rho_pad), m64.data(), p->lpc_mult);
+            } else {
+                std::vector<float2> m32((nts + 1) * nr);
+                for (size_t i = 0; i < m32.size(); ++i) m32[i] = make_float2(float(m64[2 * i]), float(m64[2 * i + 1]));
+                ck(cudaMemcpy(p->lpc_mult, m32.data(), m32.size() * sizeof(float2), cudaMemcpyHostToDevice),
+                   "upload lp_convolve multipliers");
+            }
+        }
+        run_device(p, lpc_chunk, d_in, d_out, batch, size_t(rows) * nr, size_t(rows) * nr, stream);
     });
 }
 

@@ -1036,6 +1036,32 @@ __global__ void LPR_LB(F) k_theta_fwd_T(const __grid_constant__ DevGeom g, const
     store_half_spectra<F>(result_slots<F>(smem, E, res), L2, nts, n, l0b, out);
 }
 
+// lp_convolve stage 1: theta FFT of a real doubled-grid
+// raster (2 nts rows in natural periodic order, n_rho columns, row stride
+// n_rho), two columns per complex transform, half spectra k in [0, nts] out.
+template <class F>
+__global__ void LPR_LB(F) k_lpc_theta_fwd(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                          const float* __restrict__ data, float2* __restrict__ spec) {
+    extern __shared__ float2 smem[];
+    constexpr int P = F::kP;
+    const Group<F> G;
+    const int E = F::elems(fd);
+    const int b = blockIdx.z;
+    const int l0b = 2 * P * blockIdx.x;
+    const int nts = g.nts, L2 = g.L2, n = g.n_rho;
+    const float* in = data + size_t(b) * L2 * n;
+    for (int e = threadIdx.x; e < L2 * P; e += blockDim.x) {
+        const int r = e / P, p = e % P;
+        const int l = l0b + 2 * p;
+        const float* row = in + size_t(r) * n;
+        smem[p * E + F::idx(r)] = make_float2(l < n ? row[l] : 0.f, l + 1 < n ? row[l + 1] : 0.f);
+    }
+    __syncthreads();
+    float2* sm = smem + G.g * E;
+    float2* res = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, G.tid);
+    store_half_spectra<F>(result_slots<F>(smem, E, res), L2, nts, n, l0b, spec + size_t(b) * (nts + 1) * n);
+}
+
 // R^T stage 4: Hermitian inverse over the doubled fine period (zero beyond
 // |k| < nts) and the transposed fine-grid gather G_m^T, scattering the spline
 // taps into the apron-extended coefficient image.
@@ -1342,7 +1368,8 @@ cudaError_t prepare_fft_kernels(const FftLaunch& fine, const FftLaunch& rho, con
     SET(k_theta_inv<F>, coarse.smem * coarse.per_block);    \
     SET(k_bp_theta_fwd<F>, coarse.smem * coarse.per_block); \
     SET((k_bp_theta_fwd<F, kNTheta2048>), coarse.smem * coarse.per_block); \
-    SET(k_theta_fwd_T<F>, coarse.smem * coarse.per_block)
+    SET(k_theta_fwd_T<F>, coarse.smem * coarse.per_block);  \
+    SET(k_lpc_theta_fwd<F>, coarse.smem * coarse.per_block)
     LPR_FFT_SWITCH(fine.variant, FINE)
     LPR_FFT_SWITCH(rho.variant, RHO)
     LPR_FFT_SWITCH(coarse.variant, COARSE)
@@ -1423,6 +1450,13 @@ void launch_bp_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const D
         return;
     }
 #define CALL(F) k_bp_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, qg, spec)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+}
+
+void launch_lpc_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                          const float* data, float2* spec) {
+#define CALL(F) k_lpc_theta_fwd<F><<<theta_grid(grid, L), L.threads, L.smem * L.per_block, st>>>(g, fd, data, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }

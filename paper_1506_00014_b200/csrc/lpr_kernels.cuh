@@ -87,6 +87,8 @@ void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevG
                       const float2* spec, float* lp);
 void launch_bp_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                          const float* qg, float2* spec);
+void launch_lpc_theta_fwd(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                          const float* data, float2* spec);
 void launch_theta_fwd_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                         const float* lp, float2* spec);
 void launch_theta_inv_fine_T(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
