@@ -215,4 +215,6 @@ def test_lp_convolve_gpu(lp, lpo, cuda, N, smooth):
     spec[nts] = 0
     bl = np.real(np.fft.ifft(spec, axis=0))
     back = lp.lp_convolve(torch.tensor(bl, dtype=torch.float32, device=cuda), one, plan, False).cpu().numpy()
-    assert np.abs(back - bl).max() <= 2e-6 * np.abs(bl).max()
+    err = lpo.rel_l2(back, bl)  # the SPEC's 1e-6 FFT round trip, in relative l2 for fp32 transforms
+    print(f"lp_convolve N={N}: spectrum = 1 round trip rel_l2 {err:.2e}")
+    assert err <= 1e-6

@@ -127,9 +127,14 @@ def test_file_pipelines_match_the_library(cli, lp, lpo, cuda, tmp_path):
     rec = lpt1.read_container(tmp_path / "fbp.lpt").data
     inside = np.add.outer((np.arange(N) - N / 2) ** 2, (np.arange(N) - N / 2) ** 2) < (0.45 * N) ** 2
     assert np.linalg.norm((rec - f)[inside]) / np.linalg.norm(f[inside]) < 0.3
+    # EM needs g >= 0: the clipped sinogram; a negative one is refused
+    r = run(cli, "em", "--in", s, "--iters", 3, "--out", tmp_path / "bad.lpt", ok=False)
+    assert r.returncode == 1 and "nonnegative" in r.stderr
+    sp = tmp_path / "s_pos.lpt"
+    lpt1.write_container(sp, lpt1.Container("sinogram", np.maximum(sc.data, 0), sc.grid, sc.meta))
     e1, e2 = tmp_path / "e1.lpt", tmp_path / "e2.lpt"
-    run(cli, "em", "--in", s, "--iters", 3, "--out", e1)
-    run(cli, "em", "--in", s, "--iters", 3, "--seed", 7, "--out", e2)
+    run(cli, "em", "--in", sp, "--iters", 3, "--out", e1)
+    run(cli, "em", "--in", sp, "--iters", 3, "--seed", 7, "--out", e2)
     c1, c2 = lpt1.read_container(e1), lpt1.read_container(e2)
     np.testing.assert_array_equal(c1.data, c2.data)  # deterministic
     ll = c1.meta["loglik"]
