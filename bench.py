@@ -493,7 +493,7 @@ def run_ours(args):
 
     e2e_pipelined(2)  # warm-up
     barrier()
-    e2e_pipe_k = max(8, 2 * args.steps)  # a longer stream amortises the pipeline fill and drain
+    e2e_pipe_k = max(4, min(2 * args.steps, 8))
     e2e_pipe_s = max_over_ranks(e2e_pipelined(e2e_pipe_k))
     plan2.close()
     e2e_value = ws * B / e2e_pipe_s

@@ -109,6 +109,13 @@ void host_fft(std::vector<cd>& x) {
 
 using namespace lpr;
 
+#ifndef LPR_HOST_CHUNKS
+#define LPR_HOST_CHUNKS 16  // pipeline depth of the pinned host path (chunks per call)
+#endif
+#ifndef LPR_HOST_SLOTS
+#define LPR_HOST_SLOTS 4  // device staging slots of the pinned host path
+#endif
+
 struct lpr_gpu_plan {
     int device = 0;
     lpr_geometry geo{};
@@ -136,7 +143,7 @@ struct lpr_gpu_plan {
     float *h_in = nullptr, *h_out = nullptr;   // pinned
     cudaStream_t stream = nullptr;
     cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams
-    static constexpr int kHostChunks = 16;          // pipeline depth of the pinned host path (4/8/16 measured 684/798/813 e2e)
+    static constexpr int kHostChunks = LPR_HOST_CHUNKS;          // pipeline depth of the pinned host path (4/8/16 measured 684/798/813 e2e)
     // Calls share the scratch above, so they are serialised: the mutex covers
     // the host side of a call (enqueue, host staging), and ev_done, recorded on
     // the stream of the call that last used the scratch, orders its device work
@@ -144,7 +151,7 @@ struct lpr_gpu_plan {
     std::recursive_mutex mu;
     cudaEvent_t ev_done = nullptr;
     bool has_done = false;
-    static constexpr int kHostSlots = 4;  // device staging slots of the pinned host pipeline
+    static constexpr int kHostSlots = LPR_HOST_SLOTS;  // device staging slots of the pinned host pipeline
     cudaEvent_t ev_h2d[kHostSlots] = {}, ev_comp[kHostSlots] = {}, ev_d2h[kHostSlots] = {};
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     bool tex_gather = false;      // LPR_PLAN_TEXTURE_GATHER ablation
