@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--profile-reps", type=int, default=5)
     ap.add_argument("--dry-run", action="store_true", help="gloo on CPU: rank/shard/gather plumbing only")
     ap.add_argument("--no-default-plan", action="store_true", help="skip the default-plan (minimal N_rho) row")
+    ap.add_argument("--stack", type=int, default=2048,
+                    help="config 4: slices of the whole stack sharded over the ranks (0 skips the row)")
     return ap.parse_args()
 
 
@@ -396,6 +398,37 @@ def run_ours(args):
                        f"{B} sinograms to rank 0, device events, max over ranks"}
     del gather_out
 
+    # config 4 (BASELINE.json): the whole 2048-slice stack sharded over the
+    # ranks, each rank's contiguous shard device resident (distinct slices,
+    # 34 GB at one GPU), R then R# chunk by chunk (B slices per launch)
+    stack = None
+    if args.stack > 0:
+        s_start, s_count = stack_shard(args.stack, ws, rank)
+        stack_in = phantoms.stack(g.N, s_count, seed0=0x5EED + s_start, device=dev) if s_count else None
+        torch.cuda.synchronize()
+
+        def stack_job():
+            for c0 in range(0, s_count, B):
+                nb = min(B, s_count - c0)
+                x = stack_in[c0:c0 + nb]
+                lp._lib.check(L.lpr_gpu_radon(h, x.data_ptr(), sino.data_ptr(), nb, sp))
+                lp._lib.check(L.lpr_gpu_backproject(h, sino.data_ptr(), back.data_ptr(), nb, sp))
+
+        barrier()
+        sa, sb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sa.record(stream)
+        stack_job()
+        sb.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_stack = max_over_ranks(sa.elapsed_time(sb))
+        stack = {"slices": args.stack, "slices_per_rank": s_count, "chunk": B, "ms": ms_stack,
+                 "value": args.stack / (ms_stack / 1e3), "unit": UNIT,
+                 "how": "the whole stack sharded contiguously over the ranks, each shard device resident "
+                        "(distinct Shepp-Logan / random-disc slices), R then R# per chunk of B slices, "
+                        "device events, max over ranks, one pass (no warm-up beyond the main run's)"}
+        del stack_in
+
     # R-only / R#-only throughput (same buffers, device events)
     def timed(fn, n=5, warm=1):
         for _ in range(warm):
@@ -579,6 +612,7 @@ def run_ours(args):
                          * B / (ms_step * 1e-3) / 1e9 / peak},
             "stages": stages,
             "gathered": gathered,
+            "stack": stack,
             "default_plan": default_plan,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
@@ -612,14 +646,22 @@ def run_dry(args):
     sino = sino.contiguous()
     slowest = sharding.max_over_ranks(float(rank))
     out = sharding.gather_to_root(sino, 0)
+    # the config-4 stack split: every slice of [0, stack) on exactly one rank
+    s_start, s_count = sharding.stack_shard(args.stack, ws, rank)
+    mine = torch.zeros(max(args.stack, 1), dtype=torch.int32)
+    mine[s_start:s_start + s_count] = 1
+    if ws > 1:
+        dist.all_reduce(mine)
+    stack_ok = bool((mine[:args.stack] == 1).all())
     line = None
     if rank == 0:
         ok = out is not None and out.shape[0] == B * ws and all(
-            bool((out[i] == i).all()) for i in range(B * ws))
+            bool((out[i] == i).all()) for i in range(B * ws)) and stack_ok
         line = {"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": ws, "dry_run": True, "backend": "gloo",
                 "config": {"N": N, "n_theta": n_theta, "global_batch": B * ws,
                            "parallelism": f"slices sharded dp{ws}"},
                 "gathered": {"bytes_to_rank0_per_step": (ws - 1) * B * n_theta * N * 4, "verified": ok},
+                "stack": {"slices": args.stack, "slices_per_rank0": s_count, "partition_verified": stack_ok},
                 "max_over_ranks": slowest}
         print(json.dumps(line), flush=True)
         if not ok:

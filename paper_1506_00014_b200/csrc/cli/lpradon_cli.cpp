@@ -11,6 +11,7 @@
 //   lpradon kernel-dump --size N [--sectors M] [--ntheta T] [--nrho R] --kind radon|backprojection --out F
 //   lpradon bench --sizes N1,N2,... --json F [--sectors M] [--reps K]
 //   lpradon inspect --in F [--out G]      (header to stdout; G = the re-encoded container)
+//   lpradon calibrate-cnorm [--size N] [--filter K]   (tools/calibrate_cnorm: the disc calibration)
 // Global: --device D (default 0), --threads T (accepted; the host work is GPU-side).
 // Exit 0 on success, 1 with a message on a runtime error, 2 with the usage
 // text on an unknown subcommand or flag, 3 / 4 / 5 / 6 on a bad-magic /
@@ -43,6 +44,7 @@ const char* kUsage =
     "  kernel-dump --size N [--sectors M] [--ntheta T] [--nrho R] --kind radon|backprojection --out F\n"
     "  bench --sizes N1,N2,... --json F [--sectors M] [--reps K]\n"
     "  inspect --in F [--out G]\n"
+    "  calibrate-cnorm [--size N] [--filter ramp|shepp-logan|cosine] [--sectors M]\n"
     "global flags: --device D, --threads T\n";
 
 struct Usage : std::runtime_error {
@@ -341,6 +343,45 @@ int cmd_bench(const Args& a) {
     return 0;
 }
 
+// c_norm calibration (SPEC.md:378 DESIGN DECISIONS; the reference's
+// tools/calibrate_cnorm.cpp is an empty main): the analytic sinogram of the
+// centred disc of physical radius 0.5 (raster radius 1/4, line integral
+// 2 sqrt(1/16 - s^2)), filtered back-projected with the built-in c_norm = 1/2;
+// the interior mean (physical radius < 0.4) should be 1, and c_norm = 1/2 /
+// mean is what the calibration would fix.
+int cmd_calibrate_cnorm(const Args& a) {
+    const int N = int(a.num("size", 256));
+    const std::string f = a.str("filter", "ramp");
+    const int kind = f == "ramp" ? 0 : f == "shepp-logan" ? 1 : f == "cosine" ? 2 : -1;
+    if (kind < 0) throw Usage("--filter must be ramp, shepp-logan or cosine");
+    const lpr_geometry g = geometry(N, int(a.num("sectors", 3)), 0, int(a.num("nrho", 0)));
+    Plan plan(int(a.num("device", 0)), g);
+    std::vector<float> sino(std::size_t(g.n_theta) * N), img(std::size_t(N) * N);
+    for (int i = 0; i < g.n_theta; ++i)
+        for (int j = 0; j < N; ++j) {
+            const double s = -0.5 + double(j) / N;
+            sino[std::size_t(i) * N + j] = std::abs(s) < 0.25 ? float(2.0 * std::sqrt(0.0625 - s * s)) : 0.f;
+        }
+    ck(lpr_gpu_fbp_host(plan.p, kind, sino.data(), img.data(), 1), "fbp");
+    double mean = 0.0;
+    long cnt = 0;
+    for (int r = 0; r < N; ++r)
+        for (int c = 0; c < N; ++c) {
+            const double x = -0.5 + double(c) / N, y = -0.5 + double(r) / N;
+            if (x * x + y * y < 0.04) mean += img[std::size_t(r) * N + c], ++cnt;
+        }
+    mean /= double(cnt);
+    Json out = Json::object();
+    out["N"] = Json(N);
+    out["filter"] = f;
+    out["c_norm_builtin"] = Json(0.5);
+    out["interior_mean"] = Json(mean);
+    out["c_norm_calibrated"] = Json(0.5 / mean);
+    out["within_spec"] = Json(std::abs(mean - 1.0) <= 0.05);  // mean in [0.95, 1.05]
+    std::printf("%s\n", out.dump().c_str());
+    return std::abs(mean - 1.0) <= 0.05 ? 0 : 1;
+}
+
 int cmd_inspect(const Args& a) {
     const Container c = lpr::io::read_container(a.str("in"));
     Json h = Json::object();
@@ -372,6 +413,7 @@ int main(int argc, char** argv) {
         {"kernel-dump", {{"size", "sectors", "ntheta", "nrho", "kind", "out"}, cmd_kernel_dump}},
         {"bench", {{"sizes", "json", "sectors", "reps"}, cmd_bench}},
         {"inspect", {{"in", "out"}, cmd_inspect}},
+        {"calibrate-cnorm", {{"size", "filter", "sectors", "nrho"}, cmd_calibrate_cnorm}},
     };
     auto it = cmds.find(sub);
     if (it == cmds.end()) {

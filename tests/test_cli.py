@@ -156,3 +156,12 @@ def test_bench_report(cli, tmp_path, cuda):
     dev = [sum(r["stages_ms"]["radon"].values()) for r in sizes]
     assert dev[0] < dev[1] < dev[2], dev  # device time grows with N
     assert set(sizes[0]["stages_ms"]["radon"]) >= {"prefilter_2d", "rho_pass", "theta_inv", "radon_out"}
+
+
+@pytest.mark.gpu
+def test_calibrate_cnorm(cli, cuda):
+    """tools/calibrate_cnorm: FBP of the analytic disc sinogram at
+    N=256 has interior mean 1 to 5 % with the built-in c_norm = 1/2."""
+    r = run(cli, "calibrate-cnorm", "--size", 256)
+    rep = json.loads(r.stdout)
+    assert rep["within_spec"] and abs(rep["c_norm_calibrated"] - 0.5) <= 0.025, rep

@@ -103,3 +103,5 @@ def test_bench_dry_run_two_ranks():
     assert line["gathered"]["verified"] is True
     assert line["gathered"]["bytes_to_rank0_per_step"] == 3 * 48 * 32 * 4
     assert line["max_over_ranks"] == 1.0
+    # the config-4 stack (2048 slices) split over the ranks: contiguous, disjoint, complete
+    assert line["stack"] == {"slices": 2048, "slices_per_rank0": 1024, "partition_verified": True}
