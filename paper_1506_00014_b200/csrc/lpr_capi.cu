@@ -1109,8 +1109,10 @@ int lpr_gpu_lp_convolve(lpr_gpu_plan* p, const double* spectrum, int divide_bspl
         if (!p || !spectrum) throw std::invalid_argument("lp_convolve: null plan or spectrum");
         const lpr_geometry& G = p->geo;
         const long nts = G.nts, nr = G.n_rho, rows = 2 * nts;
+        // held until the kernels are enqueued: another call must not replace the
+        // multipliers in between (run_device's Call re-locks the recursive mutex)
+        const std::lock_guard<std::recursive_mutex> lk(p->mu);
         {
-            const std::lock_guard<std::recursive_mutex> lk(p->mu);
             ck(cudaSetDevice(p->device), "cudaSetDevice");
             if (p->has_done) ck(cudaEventSynchronize(p->ev_done), "cudaEventSynchronize");  // lpc_mult is free
             // multipliers on the half theta spectrum: S(k, v) [/ (Bhat(k) Bhat(v))] / (2 nts n_rho),
@@ -1148,8 +1150,8 @@ int lpr_gpu_profile_stages_host(lpr_gpu_plan* p, int op, const float* h_in, int 
         if (!p || !h_in || batch < 1 || batch > p->max_batch) throw std::invalid_argument("profile: bad arguments");
         const lpr_geometry& G = p->geo;
         const size_t n = size_t(batch) * (op == 0 ? size_t(G.N) * G.N : size_t(G.n_theta) * G.N);
+        const std::lock_guard<std::recursive_mutex> lk(p->mu);  // the staged input stays ours through the profile
         {
-            const std::lock_guard<std::recursive_mutex> lk(p->mu);
             ck(cudaSetDevice(p->device), "cudaSetDevice");
             if (p->has_done) ck(cudaStreamWaitEvent(p->stream, p->ev_done, 0), "cudaStreamWaitEvent");
             ck(cudaMemcpyAsync(p->d_in, h_in, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "H2D");
