@@ -130,6 +130,9 @@ struct lpr_gpu_plan {
     float2* mult_RT = nullptr;   // conj(mult_R): the transposed rho multiplier
     int rho_pad = 0;             // padded rho-convolution length (non-smooth N_rho), 0: none
     bool rho_direct = false;     // N_rho == that compile-time length: same kernel, plain multipliers
+    bool rho_pad_gen = false;    // rho_pad without a compile-time padded kernel: k_rho_pad_gen over d_rho_pad
+    FftDesc d_rho_pad{};
+    FftLaunch l_rho_pad{};
     float2 *pad_R = nullptr, *pad_B = nullptr, *pad_RT = nullptr;  // its multipliers, (nts + 1) x rho_pad
     float2* lpc_mult = nullptr;  // lp_convolve: the call's multipliers ((nts + 1) x (rho_pad or n_rho))
     float* lpc_out = nullptr;    // lp_convolve: theta-inverse output, max_batch x 2 nts x lps
@@ -227,7 +230,8 @@ struct lpr_gpu_plan {
             d.twp_inv = upload(rho_stream_inv_twiddles(launch.variant));
             launch.rho_stream = 1;
         }
-        const bool padded = staged_row && launch.variant == kFftGeneric && rho_pad_length(int(n)) > 0;  // k_rho_pad
+        // a non-smooth rho length runs padded (k_rho_pad / k_rho_pad_gen), never through this descriptor
+        const bool padded = staged_row && launch.variant == kFftGeneric && d.nb != 0;
         if (!padded && (launch.smem * launch.per_block > 227 * 1024 ||
                         (staged_row && launch.smem + size_t(n) * sizeof(float2) > 227 * 1024)))
             throw std::invalid_argument("fft: a length-" + std::to_string(n) + " transform does not fit in shared memory (for a non-7-smooth n_rho this large, use the 7-smooth plan: lpr_smooth_n_rho)");
@@ -370,6 +374,18 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
     // the plain multipliers (no padding)
     p->rho_direct = p->l_rho.variant == kFftGeneric && rho_direct_length() == size_t(nr);
     if (p->rho_direct) ck(prepare_rho_pad(), "rho pad smem attribute");
+    // a runtime-radix length within a factor ~2 of the compile-time 4374 = 2 3^7 (e.g. 2187 = 3^7,
+    // the N = 1024 plans) also runs padded: the compile-time transform of twice the length measured
+    // faster than the runtime Stockham (R# at N = 1024: 1.70e-4 -> 1.54e-4 s per slice)
+    const bool near_ct = 2 * nr - 1 <= 4374 && 4374 <= 2.05 * double(nr);
+    if (p->l_rho.variant == kFftGeneric && !p->rho_pad && !p->rho_direct && (p->d_rho.nb != 0 || near_ct)) {
+        // any other non-smooth N_rho (Bluestein otherwise): padded over the next 7-smooth length
+        p->rho_pad = near_ct ? 4374 : int(smooth_at_least(2 * nr - 1));
+        p->rho_pad_gen = true;
+        p->build_desc(p->rho_pad, p->d_rho_pad, p->l_rho_pad, true);
+        p->l_rho_pad.rho_stream = 0;  // one row per block (k_rho_pad_gen)
+        ck(prepare_rho_pad_gen(p->l_rho_pad, p->rho_pad), "rho pad smem attribute");
+    }
     if (p->rho_pad) {
         const long rr = nts + 1, nb = p->rho_pad;
         std::vector<double> m64(2 * rr * nr);
@@ -393,7 +409,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
             *dst[w] = p->dalloc<float2>(size_t(rr) * nb);
             rho_pad_multipliers(p->device, int(rr), int(nr), int(nb), m64.data(), *dst[w]);
         }
-        ck(prepare_rho_pad(), "rho pad smem attribute");
+        if (!p->rho_pad_gen) ck(prepare_rho_pad(), "rho pad smem attribute");
     }
 
     // FBP transfer functions: DFT of the band-limited discrete
@@ -552,7 +568,11 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
 void rho_chunk(lpr_gpu_plan* p, int which, int nb, cudaStream_t st, const DevGeom& g, float2* spec) {
     const dim3 grid(g.nts + 1, nb * g.M);
     if (p->rho_pad) {
-        launch_rho_pad(p->rho_pad, grid, st, g, which == 0 ? p->pad_R : which == 1 ? p->pad_B : p->pad_RT, spec);
+        const float2* m = which == 0 ? p->pad_R : which == 1 ? p->pad_B : p->pad_RT;
+        if (p->rho_pad_gen)
+            launch_rho_pad_gen(p->l_rho_pad, grid, st, g, p->d_rho_pad, m, spec);
+        else
+            launch_rho_pad(p->rho_pad, grid, st, g, m, spec);
         return;
     }
     if (p->rho_direct) {
@@ -723,7 +743,9 @@ void lpc_chunk(lpr_gpu_plan* p, const float* in, float* out, int nb, cudaStream_
     const int nr = g.n_rho, rows = g.L2;
     launch_lpc_theta_fwd(p->l_coarse, dim3(cdiv(nr, 2), 1, nb), st, g, p->d_coarse, in, p->spec);
     const dim3 grid(g.nts + 1, nb);
-    if (p->rho_pad)
+    if (p->rho_pad_gen)
+        launch_rho_pad_gen(p->l_rho_pad, grid, st, g, p->d_rho_pad, p->lpc_mult, p->spec);
+    else if (p->rho_pad)
         launch_rho_pad(p->rho_pad, grid, st, g, p->lpc_mult, p->spec);
     else if (p->rho_direct)
         launch_rho_pad(int(rho_direct_length()), grid, st, g, p->lpc_mult, p->spec);

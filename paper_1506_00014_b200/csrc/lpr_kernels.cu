@@ -721,6 +721,39 @@ __global__ void LPR_LB(F) k_rho_pass(const __grid_constant__ DevGeom g, const __
     for (int j = tid; j < n; j += T) row[j] = a[F::idx(j)];
 }
 
+// Padded rho pass for a non-smooth N_rho without a compile-time padded
+// kernel (the reference plans at N = 256 / 512 / 1024: N_rho = 541, 1083,
+// 2166): the circular convolution of period N_rho as the first N_rho outputs
+// of a zero-padded linear one over the 7-smooth length fd.n >= 2 N_rho - 1
+// (padded multipliers from rho_pad_multipliers), through the runtime Stockham
+// or a compile-time plan of that length: two FFTs of the padded length per
+// row instead of Bluestein's four.
+template <class F>
+__global__ void LPR_LB(F) k_rho_pad_gen(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
+                                        const float2* __restrict__ mult, float2* __restrict__ spec) {
+    extern __shared__ float2 sm[];
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int k = blockIdx.x, item = blockIdx.y;
+    const int n = g.n_rho, nb = F::kT > 0 ? F::kN : fd.n;
+    float2* ms = sm + F::elems(fd);
+    float2* row = spec + (size_t(item) * (g.nts + 1) + k) * n;
+    const float2* mrow = mult + size_t(k) * nb;
+    for (int j = tid; j < n; j += T) __pipeline_memcpy_async(sm + F::idx(j), row + j, sizeof(float2));
+    __pipeline_commit();
+    for (int j = n + tid; j < nb; j += T) sm[F::idx(j)] = make_float2(0.f, 0.f);
+    for (int j = tid; j < nb; j += T) __pipeline_memcpy_async(ms + j, mrow + j, sizeof(float2));
+    __pipeline_commit();
+    __pipeline_wait_prior(1);
+    __syncthreads();
+    float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, tid);
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    for (int j = tid; j < nb; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], ms[j]);
+    __syncthreads();
+    a = F::template run<true>(a, a == sm ? fft_scratch<F>(sm, fd) : sm, fd, tid);
+    for (int j = tid; j < n; j += T) row[j] = a[F::idx(j)];
+}
+
 // ---- TMA bulk copies (cp.async.bulk, non-tensor) and mbarriers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1434,6 +1467,25 @@ void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGe
 #define CALL(F) k_rho_pass<F><<<grid, L.tpt, L.smem + size_t(g.n_rho) * sizeof(float2), st>>>(g, fd, mult, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
+}
+
+void launch_rho_pad_gen(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                        const float2* mult_pad, float2* spec) {
+    const int nb = fd.n;
+#define CALL(F) k_rho_pad_gen<F><<<grid, L.tpt, L.smem + size_t(nb) * sizeof(float2), st>>>(g, fd, mult_pad, spec)
+    LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+}
+
+cudaError_t prepare_rho_pad_gen(const FftLaunch& L, int nb) {
+    const size_t bytes = L.smem + size_t(nb) * sizeof(float2);
+    cudaError_t e = cudaSuccess;
+#define SETG(F)                                                                          \
+    e = cudaFuncSetAttribute(k_rho_pad_gen<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             int(bytes))
+    LPR_FFT_SWITCH(L.variant, SETG)
+#undef SETG
+    return e;
 }
 
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,

@@ -81,6 +81,9 @@ size_t rho_pad_length(int n_rho);  // padded convolution length for a non-smooth
 size_t rho_direct_length();       // the compile-time length k_rho_pad also runs unpadded
 void launch_rho_pad(int nb, dim3 grid, cudaStream_t st, const DevGeom& g, const float2* mult_pad, float2* spec);
 cudaError_t prepare_rho_pad();
+void launch_rho_pad_gen(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
+                        const float2* mult_pad, float2* spec);
+cudaError_t prepare_rho_pad_gen(const FftLaunch& L, int nb);
 void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                      const float2* mult, float2* spec);
 void launch_theta_inv(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
