@@ -211,8 +211,10 @@ __host__ __device__ constexpr int pad_walk_off(int r) {
 }
 
 // One in-place pass of radix R at Stockham stride NS over a padded buffer.
-template <int N, int T, int S, int R, int NS, int OFF, bool INV, int BAND = 0, class TW>
-__device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, int tid) {
+// PIN (first pass of a zero-padded transform): elements at or past n_in are
+// zero and are neither read nor required to be in the buffer.
+template <int N, int T, int S, int R, int NS, int OFF, bool INV, int BAND = 0, bool PIN = false, class TW>
+__device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, int tid, int n_in = N) {
     static_assert(BAND == 0 || NS * R * 2 == N, "band pruning applies to the pass before a final radix 2");
     constexpr int B = N / R;
     constexpr int NB = (B + T - 1) / T;
@@ -221,7 +223,11 @@ __device__ __forceinline__ void ct_pass(float2* x, const TW* __restrict__ twp, i
     for (int i = 0; i < NB; ++i) {
         const int b = tid + i * T;
         if (b < B) {
-            if constexpr (pad_walk_ok<S, B, R>()) {
+            if constexpr (PIN) {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    v[i][r] = b + r * B < n_in ? x[ct_pad<S>(b + r * B)] : make_float2(0.f, 0.f);
+            } else if constexpr (pad_walk_ok<S, B, R>()) {
                 const float2* xb = x + ct_pad<S>(b);
 #pragma unroll
                 for (int r = 0; r < R; ++r) v[i][r] = xb[pad_walk_off<S, B>(r)];
@@ -514,7 +520,9 @@ struct RhoStream4 {
 #else
         const TwSincos *twf = nullptr, *twi = nullptr;
 #endif
-        ct_pass<N, T, S, R1, 1, 0, false>(x, twf, tid);
+        // the first pass reads only the n_out data elements: a zero-padded
+        // convolution (k_rho_pad) leaves the rest of the buffer unwritten
+        ct_pass<N, T, S, R1, 1, 0, false, 0, true>(x, twf, tid, n_out);
         ct_pass<N, T, S, R2, R1, 0, false>(x, twf, tid);
         ct_pass<N, T, S, R3, R1 * R2, R1 * (R2 - 1), false>(x, twf, tid);
         ct_mid_fused<N, T, S, R4, R1 * (R2 - 1) + R1 * R2 * (R3 - 1)>(x, twf, ms, tid);

@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(F::kT, F::kT >= 1024 ? 1 : 2) k_rho_pad(const 
     extern __shared__ __align__(16) float2 sm[];
     const int k = blockIdx.x, item = blockIdx.y, n = g.n_rho, tid = threadIdx.x;
     float2* row = spec + (size_t(item) * (g.nts + 1) + k) * n;
-    for (int j = tid; j < F::kN; j += F::kT) sm[j] = j < n ? row[j] : make_float2(0.f, 0.f);
+    for (int j = tid; j < n; j += F::kT) sm[j] = row[j];  // [n, kN) is zero: the first pass does not read it
     __syncthreads();
     F::convolve(sm, nullptr, nullptr, mult_pad + size_t(k) * F::kN, row, tid, n);
 }
