@@ -444,6 +444,31 @@ __device__ __forceinline__ void load_packed_hermitian(Slots sm, const float2* __
             }
             return;
         }
+        if (l0 + 2 * P <= n) {
+            // odd n (the reference plans' N_rho, e.g. 4333): rows are only 8-byte
+            // aligned, so two 8-byte loads per row, still U rows in flight
+            const float2* src = in + l;
+            for (int kb = k0; kb < kmax; kb += U * RS) {
+                float2 a[U], c[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = kb + u * RS;
+                    if (k < kmax) {
+                        a[u] = __ldg(src + size_t(k) * n);
+                        c[u] = __ldg(src + size_t(k) * n + 1);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = kb + u * RS;
+                    if (k < kmax) {
+                        dst[F::idx(k)] = make_float2(a[u].x - c[u].y, a[u].y + c[u].x);
+                        if (k > 0) dst[F::idx(L - k)] = make_float2(a[u].x + c[u].y, c[u].x - a[u].y);
+                    }
+                }
+            }
+            return;
+        }
     }
 #ifndef LPR_HERM_U
 #define LPR_HERM_U 8
