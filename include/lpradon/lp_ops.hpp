@@ -38,6 +38,12 @@ struct RadonPlan {
 RadonPlan make_radon_plan(const GeometryPlan& geom, KernelMethod method = KernelMethod::quadrature,
                           int device = 0, int max_batch = 1);
 
+/// lp_convolve: Re IFFT2(FFT2(data) * spectrum [/ Bhat]) on the doubled grid
+/// (2 N_theta_sector x N_rho, rows in periodic order), on the plan's device; the spectrum's
+/// theta-Nyquist row is treated as zero, as Algorithms 1-2 do. Shape mismatch: invalid_argument.
+Array2D<double> lp_convolve(const Array2D<double>& data, const KernelSpectrum& spectrum, bool divide_bspline,
+                            const RadonPlan& plan);
+
 /// Algorithm 1.
 Sinogram fast_radon(const Image& image, const RadonPlan& plan);
 /// Algorithm 2.

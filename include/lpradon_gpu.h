@@ -116,6 +116,8 @@ int lpr_gpu_radon_transpose(lpr_gpu_plan* plan, const float* d_sino, float* d_im
  * own theta / rho / theta-inverse kernels; batch may exceed max_batch. */
 int lpr_gpu_lp_convolve(lpr_gpu_plan* plan, const double* spectrum_re_im, int divide_bspline, const float* d_in,
                         float* d_out, int batch, void* stream);
+int lpr_gpu_lp_convolve_host(lpr_gpu_plan* plan, const double* spectrum_re_im, int divide_bspline, const float* h_in,
+                             float* h_out, int batch);
 
 /* Filtered back-projection (the main caller of R#):
  * kind 0 = ramp, 1 = Shepp-Logan, 2 = cosine transfer functions along s

@@ -58,6 +58,8 @@ EXPORTS = {
                                                    ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_char_p)]),
     "lpr_gpu_lp_convolve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+    "lpr_gpu_lp_convolve_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_int]),
     "lpr_gpu_launch_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_fft_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_last_error": (ctypes.c_char_p, []),

@@ -56,6 +56,21 @@ RadonPlan make_radon_plan(const GeometryPlan& geom, KernelMethod method, int dev
     return plan;
 }
 
+Array2D<double> lp_convolve(const Array2D<double>& data, const KernelSpectrum& spectrum, bool divide_bspline,
+                            const RadonPlan& plan) {
+    const std::size_t rows = 2 * std::size_t(plan.geom.N_theta_sector), cols = std::size_t(plan.geom.N_rho);
+    require(data.rows() == rows && data.cols() == cols, "lp_convolve: data is not the plan's doubled grid");
+    require(spectrum.coeffs.rows() == rows && spectrum.coeffs.cols() == cols,
+            "lp_convolve: spectrum does not match the plan");
+    const std::vector<float> in = to_f32(data);
+    std::vector<float> res(in.size());
+    check(lpr_gpu_lp_convolve_host(plan.gpu.get(), reinterpret_cast<const double*>(spectrum.coeffs.data()),
+                                   divide_bspline ? 1 : 0, in.data(), res.data(), 1));
+    Array2D<double> out(rows, cols);
+    from_f32(res, out);
+    return out;
+}
+
 Sinogram fast_radon(const Image& image, const RadonPlan& plan) {
     const auto& p = plan.geom;
     require(image.pixels.rows() == std::size_t(p.N) && image.pixels.cols() == std::size_t(p.N),

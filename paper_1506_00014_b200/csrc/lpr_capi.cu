@@ -829,6 +829,39 @@ void run_host(lpr_gpu_plan* p, ChunkFn fn, const float* hin, float* hout, int ba
     }
 }
 
+// lp_convolve's multipliers on the half theta spectrum: S(k, v) [/ (Bhat(k) Bhat(v))] / (2 nts n_rho),
+// the theta-Nyquist row zero as in Algorithms 1-2; padded like the plan's own when its rho pass is.
+// The caller holds the plan mutex until its kernels are enqueued.
+void set_lpc_multipliers(lpr_gpu_plan* p, const double* spectrum, int divide_bspline) {
+    if (!spectrum) throw std::invalid_argument("lp_convolve: null spectrum");
+    const lpr_geometry& G = p->geo;
+    const long nts = G.nts, nr = G.n_rho, rows = 2 * nts;
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    if (p->has_done) ck(cudaEventSynchronize(p->ev_done), "cudaEventSynchronize");  // lpc_mult is free
+    auto bhat = [](long k, long n) { return (2.0 + std::cos(2.0 * kPi * double(k) / double(n))) / 3.0; };
+    std::vector<double> m64(2 * (nts + 1) * nr, 0.0);
+    const double sc = 1.0 / (double(rows) * double(nr));
+    for (long k = 0; k < nts; ++k)
+        for (long v = 0; v < nr; ++v) {
+            const double d = divide_bspline ? sc / (bhat(k, rows) * bhat(v, nr)) : sc;
+            m64[2 * (k * nr + v)] = spectrum[2 * (k * nr + v)] * d;
+            m64[2 * (k * nr + v) + 1] = spectrum[2 * (k * nr + v) + 1] * d;
+        }
+    const long cols = p->rho_pad ? p->rho_pad : nr;
+    if (!p->lpc_mult) {
+        p->lpc_mult = p->dalloc<float2>(size_t(nts + 1) * cols);
+        p->lpc_out = p->dalloc<float>(size_t(p->max_batch) * rows * p->g.lps);
+    }
+    if (p->rho_pad) {
+        rho_pad_multipliers(p->device, int(nts + 1), int(nr), int(p->rho_pad), m64.data(), p->lpc_mult);
+    } else {
+        std::vector<float2> m32((nts + 1) * nr);
+        for (size_t i = 0; i < m32.size(); ++i) m32[i] = make_float2(float(m64[2 * i]), float(m64[2 * i + 1]));
+        ck(cudaMemcpy(p->lpc_mult, m32.data(), m32.size() * sizeof(float2), cudaMemcpyHostToDevice),
+           "upload lp_convolve multipliers");
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1128,41 +1161,24 @@ int lpr_gpu_profile_stages(lpr_gpu_plan* p, int op, const float* d_in, float* d_
 int lpr_gpu_lp_convolve(lpr_gpu_plan* p, const double* spectrum, int divide_bspline, const float* d_in, float* d_out,
                         int batch, void* stream) {
     return guard([&] {
-        if (!p || !spectrum) throw std::invalid_argument("lp_convolve: null plan or spectrum");
-        const lpr_geometry& G = p->geo;
-        const long nts = G.nts, nr = G.n_rho, rows = 2 * nts;
+        if (!p) throw std::invalid_argument("null plan");
         // held until the kernels are enqueued: another call must not replace the
         // multipliers in between (run_device's Call re-locks the recursive mutex)
         const std::lock_guard<std::recursive_mutex> lk(p->mu);
-        {
-            ck(cudaSetDevice(p->device), "cudaSetDevice");
-            if (p->has_done) ck(cudaEventSynchronize(p->ev_done), "cudaEventSynchronize");  // lpc_mult is free
-            // multipliers on the half theta spectrum: S(k, v) [/ (Bhat(k) Bhat(v))] / (2 nts n_rho),
-            // the theta-Nyquist row zero as in Algorithms 1-2
-            auto bhat = [](long k, long n) { return (2.0 + std::cos(2.0 * kPi * double(k) / double(n))) / 3.0; };
-            std::vector<double> m64(2 * (nts + 1) * nr, 0.0);
-            const double sc = 1.0 / (double(rows) * double(nr));
-            for (long k = 0; k < nts; ++k)
-                for (long v = 0; v < nr; ++v) {
-                    const double d = divide_bspline ? sc / (bhat(k, rows) * bhat(v, nr)) : sc;
-                    m64[2 * (k * nr + v)] = spectrum[2 * (k * nr + v)] * d;
-                    m64[2 * (k * nr + v) + 1] = spectrum[2 * (k * nr + v) + 1] * d;
-                }
-            const long cols = p->rho_pad ? p->rho_pad : nr;
-            if (!p->lpc_mult) {
-                p->lpc_mult = p->dalloc<float2>(size_t(nts + 1) * cols);
-                p->lpc_out = p->dalloc<float>(size_t(p->max_batch) * rows * p->g.lps);
-            }
-            if (p->rho_pad) {
-                rho_pad_multipliers(p->device, int(nts + 1), int(nr), int(p->rho_pad), m64.data(), p->lpc_mult);
-            } else {
-                std::vector<float2> m32((nts + 1) * nr);
-                for (size_t i = 0; i < m32.size(); ++i) m32[i] = make_float2(float(m64[2 * i]), float(m64[2 * i + 1]));
-                ck(cudaMemcpy(p->lpc_mult, m32.data(), m32.size() * sizeof(float2), cudaMemcpyHostToDevice),
-                   "upload lp_convolve multipliers");
-            }
-        }
-        run_device(p, lpc_chunk, d_in, d_out, batch, size_t(rows) * nr, size_t(rows) * nr, stream);
+        set_lpc_multipliers(p, spectrum, divide_bspline);
+        const size_t sz = size_t(2 * p->geo.nts) * p->geo.n_rho;
+        run_device(p, lpc_chunk, d_in, d_out, batch, sz, sz, stream);
+    });
+}
+
+int lpr_gpu_lp_convolve_host(lpr_gpu_plan* p, const double* spectrum, int divide_bspline, const float* h_in,
+                             float* h_out, int batch) {
+    return guard([&] {
+        if (!p) throw std::invalid_argument("null plan");
+        const std::lock_guard<std::recursive_mutex> lk(p->mu);
+        set_lpc_multipliers(p, spectrum, divide_bspline);
+        const size_t sz = size_t(2 * p->geo.nts) * p->geo.n_rho;
+        run_host(p, lpc_chunk, h_in, h_out, batch, sz, sz);
     });
 }
 

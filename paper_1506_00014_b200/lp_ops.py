@@ -211,7 +211,7 @@ def apply_filter(sino, plan: RadonPlan, kind: str = "ramp"):
 
 def lp_convolve(data, spectrum, plan: RadonPlan, divide_bspline: bool = True):
     """Re IFFT2(FFT2(data) * spectrum [/ Bhat]) on the doubled
-    grid, data [batch x] (2 nts) x n_rho real (CUDA tensor, or numpy -> numpy),
+    grid, data [batch x] (2 nts) x n_rho real (CUDA tensor, or host array / tensor),
     spectrum (2 nts) x n_rho complex even in k_theta (zeta / zeta#), its
     theta-Nyquist row treated as zero (as in Algorithms 1-2)."""
     g = plan.geometry
@@ -219,14 +219,10 @@ def lp_convolve(data, spectrum, plan: RadonPlan, divide_bspline: bool = True):
     s = np.ascontiguousarray(spectrum, dtype=np.complex128)
     if s.shape != shape:
         raise ValueError(f"spectrum shape {s.shape} does not match the plan {shape}")
-    if not (_is_torch(data) and data.is_cuda):
-        import torch
-
-        t = torch.as_tensor(np.ascontiguousarray(data, dtype=np.float32), device=f"cuda:{plan.device}")
-        return lp_convolve(t, s, plan, divide_bspline).cpu().numpy()
+    div = int(bool(divide_bspline))
     return _run(plan, data, shape, shape,
-                lambda h, i, o, b, st: lib().lpr_gpu_lp_convolve(h, s.ctypes.data, int(bool(divide_bspline)), i, o,
-                                                                 b, st), None)
+                lambda h, i, o, b, st: lib().lpr_gpu_lp_convolve(h, s.ctypes.data, div, i, o, b, st),
+                lambda h, i, o, b: lib().lpr_gpu_lp_convolve_host(h, s.ctypes.data, div, i, o, b))
 
 
 def fbp(sino, plan: RadonPlan, kind: str = "ramp"):

@@ -208,6 +208,9 @@ def test_lp_convolve_gpu(lp, lpo, cuda, N, smooth):
             pad = _padded_theta_convolution(z, d, nts)
             assert lpo.rel_l2(per[out_rows % rows], pad) <= 1e-5
     assert not lp.lp_convolve(torch.zeros(rows, nr, device=cuda), z, plan).any()
+    # the host-buffer entry point (lpr_gpu_lp_convolve_host) gives the device call's bits
+    host = lp.lp_convolve(data.astype(np.float32), z, plan)
+    np.testing.assert_array_equal(host, lp.lp_convolve(dev, z, plan).cpu().numpy())
     # spectrum == 1, no B-spline division: band-limited data comes back
     one = np.ones((rows, nr), complex)
     one[nts] = 0
