@@ -40,6 +40,7 @@ struct Error : std::runtime_error {
 
 void ck(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return;
+    cudaGetLastError();  // a non-sticky error must not resurface at the next launch check
     const lpr_status c = e == cudaErrorMemoryAllocation ? LPR_ERR_OOM : LPR_ERR_CUDA;
     throw Error(c, std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -136,6 +137,7 @@ struct lpr_gpu_plan {
     float2 *pad_R = nullptr, *pad_B = nullptr, *pad_RT = nullptr;  // its multipliers, (nts + 1) x rho_pad
     float2* lpc_mult = nullptr;  // lp_convolve: the call's multipliers ((nts + 1) x (rho_pad or n_rho))
     float* lpc_out = nullptr;    // lp_convolve: theta-inverse output, max_batch x 2 nts x lps
+    float *lpc_din = nullptr, *lpc_dout = nullptr;  // lp_convolve host path: device staging, max_batch rasters each
     float* band = nullptr;       // banded transpose of the apron-extended 1-D prefilter
     int band_h = 0;
     float *qf = nullptr, *tmp = nullptr, *qg = nullptr, *lp = nullptr;
@@ -1175,10 +1177,25 @@ int lpr_gpu_lp_convolve_host(lpr_gpu_plan* p, const double* spectrum, int divide
                              float* h_out, int batch) {
     return guard([&] {
         if (!p) throw std::invalid_argument("null plan");
+        if (batch < 0 || (batch > 0 && (!h_in || !h_out))) throw std::invalid_argument("bad buffers or batch");
         const std::lock_guard<std::recursive_mutex> lk(p->mu);
         set_lpc_multipliers(p, spectrum, divide_bspline);
+        // doubled-grid rasters are larger than the plan's image / sinogram staging: own device buffers
         const size_t sz = size_t(2 * p->geo.nts) * p->geo.n_rho;
-        run_host(p, lpc_chunk, h_in, h_out, batch, sz, sz);
+        if (!p->lpc_din) {
+            p->lpc_din = p->dalloc<float>(size_t(p->max_batch) * sz);
+            p->lpc_dout = p->dalloc<float>(size_t(p->max_batch) * sz);
+        }
+        cudaStream_t st = p->stream;
+        const Call call(p, st);
+        for (int b0 = 0; b0 < batch; b0 += p->max_batch) {
+            const int nb = std::min(p->max_batch, batch - b0);
+            const size_t bytes = size_t(nb) * sz * sizeof(float);
+            ck(cudaMemcpyAsync(p->lpc_din, h_in + size_t(b0) * sz, bytes, cudaMemcpyHostToDevice, st), "H2D");
+            lpc_chunk(p, p->lpc_din, p->lpc_dout, nb, st);
+            ck(cudaMemcpyAsync(h_out + size_t(b0) * sz, p->lpc_dout, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "stream sync");
+        }
     });
 }
 
