@@ -111,7 +111,7 @@ void host_fft(std::vector<cd>& x) {
 using namespace lpr;
 
 #ifndef LPR_HOST_CHUNKS
-#define LPR_HOST_CHUNKS 16  // pipeline depth of the pinned host path (chunks per call)
+#define LPR_HOST_CHUNKS 8  // pipeline depth of the pinned host path (chunks per call)
 #endif
 #ifndef LPR_HOST_SLOTS
 #define LPR_HOST_SLOTS 4  // device staging slots of the pinned host path
@@ -148,7 +148,7 @@ struct lpr_gpu_plan {
     float *h_in = nullptr, *h_out = nullptr;   // pinned
     cudaStream_t stream = nullptr;
     cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams
-    static constexpr int kHostChunks = LPR_HOST_CHUNKS;          // pipeline depth of the pinned host path (4/8/16 measured 684/798/813 e2e)
+    static constexpr int kHostChunks = LPR_HOST_CHUNKS;  // chunks per host call (round 2, 4 paired runs: 8 -> 949 vs 16 -> 921 e2e slices/s)
     // Calls share the scratch above, so they are serialised: the mutex covers
     // the host side of a call (enqueue, host staging), and ev_done, recorded on
     // the stream of the call that last used the scratch, orders its device work
