@@ -445,6 +445,14 @@ def run_ours(args):
 
     ms_r = timed(lambda: lp._lib.check(L.lpr_gpu_radon(h, imgs.data_ptr(), sino.data_ptr(), B, sp)))
     ms_b = timed(lambda: lp._lib.check(L.lpr_gpu_backproject(h, sino.data_ptr(), back.data_ptr(), B, sp)))
+    # the callers next to the path: FBP (cosine filter, c_norm R#(filter g)) and EM
+    # iterations (R, ratio, R#, update; g >= 0) on the same stack, device time per slice
+    ms_fbp = timed(lambda: lp._lib.check(L.lpr_gpu_fbp(h, 2, sino.data_ptr(), back.data_ptr(), B, sp)))
+    g_pos = sino.clamp_min(0)
+    em_iters = 3
+    ms_em = timed(lambda: lp._lib.check(L.lpr_gpu_em(h, g_pos.data_ptr(), back.data_ptr(), B, em_iters, 1, None, sp)),
+                  n=2) / em_iters
+    del g_pos
 
     # end to end through the public host API: pinned host slices in, H2D,
     # R, D2H sinogram, then H2D sinogram, R#, D2H image, every step.
@@ -593,6 +601,9 @@ def run_ours(args):
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config(args, g, ws),
             "radon_slices_per_s": ws * B / (ms_r / 1e3), "backproject_slices_per_s": ws * B / (ms_b / 1e3),
+            "fbp_slices_per_s": ws * B / (ms_fbp / 1e3),
+            "em_iterations": {"slice_iterations_per_s": ws * B / (ms_em / 1e3), "ms_per_iteration_per_slice": ms_em / B,
+                              "how": "lpr_gpu_em, 3 iterations from f0 = 1 on the disc, clamped stack sinograms"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes_img + nbytes_sino,
                     "d2h_bytes_per_step": nbytes_sino + nbytes_img,
                     "how": "lpr_gpu_radon_host of steps 0..K-1 on one host thread / plan and "
