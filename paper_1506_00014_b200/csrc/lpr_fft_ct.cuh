@@ -581,7 +581,7 @@ using Fft16384Band = CtFft<16384, 512, 1, 1, 5, 32, 32, 8>;
 // streamed rho pass for N_rho = 4374 (2 rows in flight per block, 2 blocks per SM)
 // default-plan rho pass (N_rho = 4333 = 7 * 619): the circular convolution as
 // a zero-padded linear one over 8748 = 2^2 3^7 >= 2 N_rho - 1 (k_rho_pad)
-using RhoPad8748 = RhoStream4<8748, 512, 0, 9, 9, 9, 12>;
+using RhoPad8748 = RhoStream4<8748, 486, 0, 9, 9, 9, 12>;  // 486 threads: two radix-9 butterflies each (512: 2.99, 486: 2.92 ms)
 // the reference's N = 4096 plan (N_rho = 8666 = 2 * 7 * 619) the same way over
 // 17496 = 2^3 3^7 >= 2 * 8666 - 1: one 140 KB row per block, 1024 threads
 using RhoPad17496 = RhoStream4<17496, 1024, 0, 18, 18, 6, 9>;
