@@ -583,8 +583,9 @@ using Fft16384Band = CtFft<16384, 512, 1, 1, 5, 32, 32, 8>;
 // a zero-padded linear one over 8748 = 2^2 3^7 >= 2 N_rho - 1 (k_rho_pad)
 using RhoPad8748 = RhoStream4<8748, 486, 0, 9, 9, 9, 12>;  // 486 threads: two radix-9 butterflies each (512: 2.99, 486: 2.92 ms)
 // the reference's N = 4096 plan (N_rho = 8666 = 2 * 7 * 619) the same way over
-// 17496 = 2^3 3^7 >= 2 * 8666 - 1: one 140 KB row per block, 1024 threads
-using RhoPad17496 = RhoStream4<17496, 1024, 0, 18, 18, 6, 9>;
+// 17496 = 2^3 3^7 >= 2 * 8666 - 1: one 140 KB row per block
+// 972 threads: exactly 1 / 3 / 2 butterflies per thread in the radix-18 / 6 / 9 passes (1024: 3.58, 972: 3.47 ms per 4 slices)
+using RhoPad17496 = RhoStream4<17496, 972, 0, 18, 18, 6, 9>;
 // (radix 27,27,6 at 192 threads: 1.44 ms / 16 slices; 9,9,9,6 at 512 threads: 1.49)
 #ifndef LPR_RHO_T
 #define LPR_RHO_T 192

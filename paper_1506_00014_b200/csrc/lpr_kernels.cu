@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(F::kT, 2) k_rho_stream(const __grid_constant__
 // GPU in fp64, rho_pad_multipliers). One row per block, the multiplier read
 // from L2 inside the fused middle butterfly; replaces Bluestein (15x slower).
 template <class F>
-__global__ void __launch_bounds__(F::kT, F::kT >= 1024 ? 1 : 2) k_rho_pad(const __grid_constant__ DevGeom g,
+__global__ void __launch_bounds__(F::kT, F::kT > 512 ? 1 : 2) k_rho_pad(const __grid_constant__ DevGeom g,
                                                       const float2* __restrict__ mult_pad, float2* __restrict__ spec) {
     extern __shared__ __align__(16) float2 sm[];
     const int k = blockIdx.x, item = blockIdx.y, n = g.n_rho, tid = threadIdx.x;
