@@ -32,7 +32,7 @@ constexpr std::uint32_t kVersion = 1;
 std::mutex g_mu;
 bool g_set = false;  // lpr_spectrum_cache_dir was called (overrides the environment)
 std::string g_dir;
-std::atomic<long long> g_hits{0}, g_stores{0};
+std::atomic<long long> g_hits{0}, g_stores{0}, g_tmp_seq{0};
 
 std::string cache_dir() {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -81,7 +81,8 @@ void spectrum_cache_store(const lpr_geometry& g, int kind, const double* data) {
     const std::string dir = cache_dir();
     if (dir.empty()) return;
     const std::string path = cache_path(dir, g, kind);
-    const std::string tmp = path + ".tmp" + std::to_string(long(getpid())) + "_" + std::to_string(g_stores.load());
+    // unique per process and per call, so concurrent stores (threads or ranks) never share a temporary
+    const std::string tmp = path + ".tmp" + std::to_string(long(getpid())) + "_" + std::to_string(g_tmp_seq.fetch_add(1));
     std::FILE* f = std::fopen(tmp.c_str(), "wb");
     if (!f) return;  // an unwritable cache directory only costs the recomputation
     Header h{};
