@@ -150,6 +150,10 @@ int lpr_gpu_em_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int b
 int lpr_gpu_radon_host(lpr_gpu_plan* plan, const float* h_img, float* h_sino, int batch);
 int lpr_gpu_backproject_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int batch);
 int lpr_gpu_radon_transpose_host(lpr_gpu_plan* plan, const float* h_sino, float* h_img, int batch);
+/* R then R# of the same slices in one call (the normal operator R# R of
+ * iterative reconstruction, the bench step): h_img in, both the sinograms
+ * R f (h_sino) and R# R f (h_back) out; R#'s input stays on the device. */
+int lpr_gpu_radon_backproject_host(lpr_gpu_plan* plan, const float* h_img, float* h_sino, float* h_back, int batch);
 
 /* Instrumentation: run one chunk of op (0 = R, 1 = R#) on device buffers
  * `reps` times on the plan's stream with CUDA events between the launches;

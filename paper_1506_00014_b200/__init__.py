@@ -16,6 +16,7 @@ from .lp_ops import (  # noqa: F401
     inner_image,
     inner_sinogram,
     lp_convolve,
+    radon_backproject,
     radon_transpose,
     sampling_plan,
     sensitivity_image,

@@ -60,6 +60,8 @@ EXPORTS = {
                                            ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "lpr_gpu_lp_convolve_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                                 ctypes.c_void_p, ctypes.c_int]),
+    "lpr_gpu_radon_backproject_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                      ctypes.c_void_p, ctypes.c_int]),
     "lpr_gpu_launch_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_fft_count": (ctypes.c_longlong, [ctypes.c_void_p]),
     "lpr_gpu_last_error": (ctypes.c_char_p, []),

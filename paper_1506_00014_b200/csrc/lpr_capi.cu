@@ -158,6 +158,8 @@ struct lpr_gpu_plan {
     bool has_done = false;
     static constexpr int kHostSlots = LPR_HOST_SLOTS;  // device staging slots of the pinned host pipeline
     cudaEvent_t ev_h2d[kHostSlots] = {}, ev_comp[kHostSlots] = {}, ev_d2h[kHostSlots] = {};
+    cudaEvent_t ev_mid[kHostSlots] = {};  // R done in a slot (radon_backproject_host: its sinograms may go out)
+    float* d_back = nullptr;              // radon_backproject_host: back-projection staging (max_batch images)
     cudaEvent_t* prof = nullptr;  // per-stage profiling events (lpr_gpu_profile_stages)
     bool tex_gather = false;      // LPR_PLAN_TEXTURE_GATHER ablation
     int tex_mode = 0;             // gather path of the R fine grid: 0 quad taps, 1 hardware bilinear (ablation)
@@ -249,6 +251,7 @@ struct lpr_gpu_plan {
             if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
             if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
             if (ev_d2h[i]) cudaEventDestroy(ev_d2h[i]);
+            if (ev_mid[i]) cudaEventDestroy(ev_mid[i]);
         }
         if (ev_done) cudaEventDestroy(ev_done);
         if (s_in) cudaStreamDestroy(s_in);
@@ -501,6 +504,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         ck(cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventCreateWithFlags(&p->ev_d2h[i], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&p->ev_mid[i], cudaEventDisableTiming), "cudaEventCreate");
     }
 
     ck(prepare_filter_kernel(p->l_filt), "filter smem attribute");
@@ -864,6 +868,53 @@ void set_lpc_multipliers(lpr_gpu_plan* p, const double* spectrum, int divide_bsp
     }
 }
 
+// One step of the normal operator on host buffers: R of each chunk of
+// images, its sinograms out to the host, R# of the same sinograms straight
+// from device memory, the back-projections out; H2D / compute / D2H of
+// successive chunks overlap on three streams (chunks of c slices, up to
+// kHostSlots in flight, as run_host). The sinograms never come back in.
+void run_host_normal(lpr_gpu_plan* p, const float* h_img, float* h_sino, float* h_back, int batch) {
+    if (!p) throw std::invalid_argument("null plan");
+    if (batch < 0 || (batch > 0 && (!h_img || !h_sino || !h_back))) throw std::invalid_argument("bad buffers or batch");
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    const size_t isz = size_t(p->geo.N) * p->geo.N, ssz = size_t(p->geo.n_theta) * p->geo.N;
+    cudaStream_t st = p->stream;
+    const Call call(p, st);
+    if (!p->d_back) p->d_back = p->dalloc<float>(size_t(p->max_batch) * isz);
+    const bool pinned = is_pinned(h_img) && is_pinned(h_sino) && is_pinned(h_back);
+    const int c = pinned ? std::max(1, std::min(p->max_batch / 2, (batch + lpr_gpu_plan::kHostChunks - 1) /
+                                                                      lpr_gpu_plan::kHostChunks))
+                         : p->max_batch;
+    const int slots = pinned ? std::min(lpr_gpu_plan::kHostSlots, p->max_batch / c) : 1;
+    const int chunks = (batch + c - 1) / c;
+    for (int i = 0; i < chunks; ++i) {
+        const int slot = i % slots, b0 = i * c, nb = std::min(c, batch - b0);
+        float* di = p->d_in + size_t(slot) * c * isz;
+        float* ds = p->d_out + size_t(slot) * c * ssz;
+        float* db = p->d_back + size_t(slot) * c * isz;
+        if (i >= slots) ck(cudaStreamWaitEvent(p->s_in, p->ev_comp[slot], 0), "wait");
+        ck(cudaMemcpyAsync(di, h_img + size_t(b0) * isz, size_t(nb) * isz * sizeof(float), cudaMemcpyHostToDevice,
+                           p->s_in), "H2D");
+        ck(cudaEventRecord(p->ev_h2d[slot], p->s_in), "event");
+        ck(cudaStreamWaitEvent(st, p->ev_h2d[slot], 0), "wait");
+        if (i >= slots) ck(cudaStreamWaitEvent(st, p->ev_d2h[slot], 0), "wait");
+        radon_chunk(p, di, ds, nb, st);
+        ck(cudaEventRecord(p->ev_mid[slot], st), "event");
+        backproject_chunk(p, ds, db, nb, st);
+        ck(cudaEventRecord(p->ev_comp[slot], st), "event");
+        ck(cudaStreamWaitEvent(p->s_out, p->ev_mid[slot], 0), "wait");
+        ck(cudaMemcpyAsync(h_sino + size_t(b0) * ssz, ds, size_t(nb) * ssz * sizeof(float), cudaMemcpyDeviceToHost,
+                           p->s_out), "D2H");
+        ck(cudaStreamWaitEvent(p->s_out, p->ev_comp[slot], 0), "wait");
+        ck(cudaMemcpyAsync(h_back + size_t(b0) * isz, db, size_t(nb) * isz * sizeof(float), cudaMemcpyDeviceToHost,
+                           p->s_out), "D2H");
+        ck(cudaEventRecord(p->ev_d2h[slot], p->s_out), "event");
+        if (!pinned) ck(cudaStreamSynchronize(p->s_out), "stream sync");  // pageable: one chunk at a time
+    }
+    ck(cudaStreamSynchronize(p->s_out), "stream sync");
+    ck(cudaStreamSynchronize(st), "stream sync");
+}
+
 }  // namespace
 
 extern "C" {
@@ -1068,6 +1119,10 @@ int lpr_gpu_radon_host(lpr_gpu_plan* p, const float* h_img, float* h_sino, int b
         run_host(p, radon_chunk, h_img, h_sino, batch, size_t(p ? p->geo.N : 0) * (p ? p->geo.N : 0),
                  size_t(p ? p->geo.n_theta : 0) * (p ? p->geo.N : 0));
     });
+}
+
+int lpr_gpu_radon_backproject_host(lpr_gpu_plan* p, const float* h_img, float* h_sino, float* h_back, int batch) {
+    return guard([&] { run_host_normal(p, h_img, h_sino, h_back, batch); });
 }
 
 int lpr_gpu_backproject_host(lpr_gpu_plan* p, const float* h_sino, float* h_img, int batch) {

@@ -180,6 +180,30 @@ def fast_backprojection(sino, plan: RadonPlan):
                 lib().lpr_gpu_backproject_host)
 
 
+def radon_backproject(image, plan: RadonPlan):
+    """R then R# of the same slices in one host-buffer call (the normal
+    operator of iterative reconstruction): image [batch x] N x N host array or
+    CPU tensor -> (R f, R# R f), the sinograms never re-uploaded."""
+    import torch
+
+    g = plan.geometry
+    x = image if _is_torch(image) else torch.as_tensor(np.ascontiguousarray(image, dtype=np.float32))
+    if x.is_cuda or x.dtype != torch.float32:
+        raise ValueError("expected a float32 host array or CPU tensor")
+    single = x.dim() == 2
+    xb = (x.unsqueeze(0) if single else x).contiguous()
+    if tuple(xb.shape[1:]) != (g.N, g.N):
+        raise ValueError(f"image shape {tuple(x.shape)} does not match the plan")
+    pin = xb.is_pinned()
+    sino = torch.empty((xb.shape[0], g.n_theta, g.N), dtype=torch.float32, pin_memory=pin)
+    back = torch.empty((xb.shape[0], g.N, g.N), dtype=torch.float32, pin_memory=pin)
+    check(lib().lpr_gpu_radon_backproject_host(plan.handle, xb.data_ptr(), sino.data_ptr(), back.data_ptr(),
+                                               xb.shape[0]))
+    if not _is_torch(image):
+        sino, back = sino.numpy(), back.numpy()
+    return (sino[0], back[0]) if single else (sino, back)
+
+
 def radon_transpose(sino, plan: RadonPlan):
     """Exact adjoint of fast_radon under the weighted inner products of adjoint_gap."""
     g = plan.geometry

@@ -430,3 +430,24 @@ def test_unaligned_buffers_take_the_general_path(lp, lpo, cuda):
     bs[1:] = s_al.flatten()
     su = bs[1:].view(g.n_theta, N)
     assert float((lp.fast_backprojection(s_al, plan) - lp.fast_backprojection(su, plan)).abs().max()) == 0.0
+
+
+def test_radon_backproject_one_call_matches_two(lp, lpo, cuda):
+    """lpr_gpu_radon_backproject_host (R then R# in one host call, the sinograms
+    kept on the device for R#) returns the bits of fast_radon then
+    fast_backprojection, pinned (pipelined chunks) and pageable buffers, a
+    batch above max_batch."""
+    import torch
+
+    N = 256
+    plan = lp.RadonPlan(lp.sampling_plan(N), max_batch=4)
+    f = _inputs(lpo, N, 7).astype(np.float32)
+    s_ref = lp.fast_radon(f, plan)
+    b_ref = lp.fast_backprojection(s_ref, plan)
+    s1, b1 = lp.radon_backproject(f, plan)
+    np.testing.assert_array_equal(s1, s_ref)
+    np.testing.assert_array_equal(b1, b_ref)
+    fp = torch.tensor(f).pin_memory()
+    s2, b2 = lp.radon_backproject(fp, plan)
+    np.testing.assert_array_equal(s2.numpy(), s_ref)
+    np.testing.assert_array_equal(b2.numpy(), b_ref)
