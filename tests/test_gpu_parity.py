@@ -389,7 +389,7 @@ def test_em_parity_and_properties(lp, lpo, cuda):
         lp.em_run(-sino, plan, 1)
 
 
-@pytest.mark.parametrize("M,n_theta", [(4, 0), (6, 0), (3, 200)])
+@pytest.mark.parametrize("M,n_theta", [(4, 0), (5, 0), (6, 0), (3, 200)])
 def test_parity_other_sector_counts_and_angles(lp, lpo, cuda, M, n_theta):
     """Sector counts other than 3 and a non-default angle count (rounded up to
     a multiple of 2M, geometry.cpp:69-98) run through the generic FFT lengths."""
@@ -451,3 +451,25 @@ def test_radon_backproject_one_call_matches_two(lp, lpo, cuda):
     s2, b2 = lp.radon_backproject(fp, plan)
     np.testing.assert_array_equal(s2.numpy(), s_ref)
     np.testing.assert_array_equal(b2.numpy(), b_ref)
+
+
+@pytest.mark.parametrize("N", [96, 100, 250])
+def test_parity_sizes_off_the_power_of_two_grid(lp, lpo, cuda, N):
+    """Image sizes that are not powers of two (even: sampling_plan requires it, geometry.cpp; raster pitch, prefilter
+    tiles, spline aprons and the R / R# kernels' edge handling), against the
+    oracle on the reference's own plan."""
+    import torch
+
+    g = lp.sampling_plan(N)
+    p = lpo.make_plan(N)
+    assert (g.n_theta, g.n_rho) == (p.n_theta, p.n_rho)
+    z, zb = lpo.spectrum(p, 0), lpo.spectrum(p, 1)
+    plan = lp.RadonPlan(g, z, zb, max_batch=2)
+    f = _inputs(lpo, N, 3)
+    want = lpo.fast_radon(p, z, f)
+    got = lp.fast_radon(torch.tensor(f, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    wantb = lpo.fast_backprojection(p, zb, want)
+    gotb = lp.fast_backprojection(torch.tensor(want, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    for i in range(3):
+        assert lpo.rel_l2(got[i], want[i]) <= TOL, (i, lpo.rel_l2(got[i], want[i]))
+        assert lpo.rel_l2(gotb[i], wantb[i]) <= TOL, (i, lpo.rel_l2(gotb[i], wantb[i]))
