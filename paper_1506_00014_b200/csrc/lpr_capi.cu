@@ -387,8 +387,7 @@ void init_plan(lpr_gpu_plan* p, const double* zeta, const double* zeta_bp) {
         // any other non-smooth N_rho (Bluestein otherwise): padded over the next 7-smooth length
         p->rho_pad = near_ct ? 4374 : int(smooth_at_least(2 * nr - 1));
         p->rho_pad_gen = true;
-        p->build_desc(p->rho_pad, p->d_rho_pad, p->l_rho_pad, true);
-        p->l_rho_pad.rho_stream = 0;  // one row per block (k_rho_pad_gen)
+        p->build_desc(p->rho_pad, p->d_rho_pad, p->l_rho_pad);  // one row per block, multiplier from L2
         ck(prepare_rho_pad_gen(p->l_rho_pad, p->rho_pad), "rho pad smem attribute");
     }
     if (p->rho_pad) {

@@ -760,20 +760,17 @@ __global__ void LPR_LB(F) k_rho_pad_gen(const __grid_constant__ DevGeom g, const
     const int tid = threadIdx.x, T = blockDim.x;
     const int k = blockIdx.x, item = blockIdx.y;
     const int n = g.n_rho, nb = F::kT > 0 ? F::kN : fd.n;
-    float2* ms = sm + F::elems(fd);
     float2* row = spec + (size_t(item) * (g.nts + 1) + k) * n;
-    const float2* mrow = mult + size_t(k) * nb;
+    const float2* mrow = mult + size_t(k) * nb;  // read from L2 in the multiply (no shared copy: long
+                                                  // padded rows need all of shared memory for the FFT)
     for (int j = tid; j < n; j += T) __pipeline_memcpy_async(sm + F::idx(j), row + j, sizeof(float2));
     __pipeline_commit();
     for (int j = n + tid; j < nb; j += T) sm[F::idx(j)] = make_float2(0.f, 0.f);
-    for (int j = tid; j < nb; j += T) __pipeline_memcpy_async(ms + j, mrow + j, sizeof(float2));
-    __pipeline_commit();
-    __pipeline_wait_prior(1);
-    __syncthreads();
-    float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, tid);
     __pipeline_wait_prior(0);
     __syncthreads();
-    for (int j = tid; j < nb; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], ms[j]);
+    float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, tid);
+    __syncthreads();
+    for (int j = tid; j < nb; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], __ldg(mrow + j));
     __syncthreads();
     a = F::template run<true>(a, a == sm ? fft_scratch<F>(sm, fd) : sm, fd, tid);
     for (int j = tid; j < n; j += T) row[j] = a[F::idx(j)];
@@ -1496,14 +1493,13 @@ void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGe
 
 void launch_rho_pad_gen(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                         const float2* mult_pad, float2* spec) {
-    const int nb = fd.n;
-#define CALL(F) k_rho_pad_gen<F><<<grid, L.tpt, L.smem + size_t(nb) * sizeof(float2), st>>>(g, fd, mult_pad, spec)
+#define CALL(F) k_rho_pad_gen<F><<<grid, L.tpt, L.smem, st>>>(g, fd, mult_pad, spec)
     LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
 }
 
-cudaError_t prepare_rho_pad_gen(const FftLaunch& L, int nb) {
-    const size_t bytes = L.smem + size_t(nb) * sizeof(float2);
+cudaError_t prepare_rho_pad_gen(const FftLaunch& L, int) {
+    const size_t bytes = L.smem;
     cudaError_t e = cudaSuccess;
 #define SETG(F)                                                                          \
     e = cudaFuncSetAttribute(k_rho_pad_gen<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, \

@@ -453,7 +453,7 @@ def test_radon_backproject_one_call_matches_two(lp, lpo, cuda):
     np.testing.assert_array_equal(b2.numpy(), b_ref)
 
 
-@pytest.mark.parametrize("N", [96, 100, 250])
+@pytest.mark.parametrize("N", [96, 100, 250, 1536])
 def test_parity_sizes_off_the_power_of_two_grid(lp, lpo, cuda, N):
     """Image sizes that are not powers of two (even: sampling_plan requires it, geometry.cpp; raster pitch, prefilter
     tiles, spline aprons and the R / R# kernels' edge handling), against the
@@ -473,3 +473,26 @@ def test_parity_sizes_off_the_power_of_two_grid(lp, lpo, cuda, N):
     for i in range(3):
         assert lpo.rel_l2(got[i], want[i]) <= TOL, (i, lpo.rel_l2(got[i], want[i]))
         assert lpo.rel_l2(gotb[i], wantb[i]) <= TOL, (i, lpo.rel_l2(gotb[i], wantb[i]))
+
+
+def test_parity_n3072_reference_plan(lp, lpo, cuda):
+    """N=3072 on the reference's own plan (N_rho = 6499 = 67 * 97): the rho
+    convolution padded over 13122 = 2 * 3^8 through the runtime Stockham with
+    the multiplier read from L2 (the padded row alone takes 210 KB of shared
+    memory); one slice each way against the oracle."""
+    import torch
+
+    N = 3072
+    g = lp.sampling_plan(N)
+    assert g.n_rho == 6499
+    p = lpo.make_plan(N)
+    z, zb = lpo.spectrum(p, 0), lpo.spectrum(p, 1)
+    plan = lp.RadonPlan(g, z, zb, max_batch=1)
+    f = lpo.smooth_disc_image(N, 0.9, 3072)
+    want = lpo.fast_radon(p, z, f)
+    got = lp.fast_radon(torch.tensor(f, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    wantb = lpo.fast_backprojection(p, zb, want)
+    gotb = lp.fast_backprojection(torch.tensor(want, dtype=torch.float32, device=cuda), plan).cpu().numpy()
+    er, eb = lpo.rel_l2(got, want), lpo.rel_l2(gotb, wantb)
+    print(f"N=3072 n_rho=6499: R rel_l2 {er:.3e}, R# rel_l2 {eb:.3e}")
+    assert er <= TOL and eb <= TOL
