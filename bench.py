@@ -298,10 +298,15 @@ def run_reference(args):
         cpu_sample(p, z, zb)
     dt = (time.perf_counter() - t) / args.steps
     value = 1.0 / dt
+    # the same plan and metric as the GPU arm; a CPU step is one slice (the GPU arm's is 16 per GPU)
+    ref_cfg = config(args, p, ws)
+    ref_cfg["global_batch"] = 1
+    ref_cfg["workload"] = (f"N={p.N} stack, {p.n_theta} angles, M={p.M}, step = R then R# on 1 slice "
+                           "(CPU; the GPU arm's step is 16 slices per GPU)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": warm, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": config(args, p, ws),
+        "dtype": "f64", "data": "synthetic", "config": ref_cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": CPU_SAMPLE,
                          "slices_per_step": 1},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
