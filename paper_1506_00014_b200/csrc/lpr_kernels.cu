@@ -753,7 +753,10 @@ __global__ void LPR_LB(F) k_rho_pass(const __grid_constant__ DevGeom g, const __
 // (padded multipliers from rho_pad_multipliers), through the runtime Stockham
 // or a compile-time plan of that length: two FFTs of the padded length per
 // row instead of Bluestein's four.
-template <class F>
+// STAGE: the multiplier row is staged in shared memory (cp.async, landing
+// during the forward FFT); else it is read from L2 in the multiply (long
+// padded rows need all of shared memory for the transform, e.g. 13122).
+template <class F, bool STAGE>
 __global__ void LPR_LB(F) k_rho_pad_gen(const __grid_constant__ DevGeom g, const __grid_constant__ FftDesc fd,
                                         const float2* __restrict__ mult, float2* __restrict__ spec) {
     extern __shared__ float2 sm[];
@@ -761,16 +764,23 @@ __global__ void LPR_LB(F) k_rho_pad_gen(const __grid_constant__ DevGeom g, const
     const int k = blockIdx.x, item = blockIdx.y;
     const int n = g.n_rho, nb = F::kT > 0 ? F::kN : fd.n;
     float2* row = spec + (size_t(item) * (g.nts + 1) + k) * n;
-    const float2* mrow = mult + size_t(k) * nb;  // read from L2 in the multiply (no shared copy: long
-                                                  // padded rows need all of shared memory for the FFT)
+    const float2* mrow = mult + size_t(k) * nb;
+    float2* ms = sm + F::elems(fd);
     for (int j = tid; j < n; j += T) __pipeline_memcpy_async(sm + F::idx(j), row + j, sizeof(float2));
     __pipeline_commit();
     for (int j = n + tid; j < nb; j += T) sm[F::idx(j)] = make_float2(0.f, 0.f);
-    __pipeline_wait_prior(0);
+    if constexpr (STAGE) {
+        for (int j = tid; j < nb; j += T) __pipeline_memcpy_async(ms + j, mrow + j, sizeof(float2));
+        __pipeline_commit();
+        __pipeline_wait_prior(1);
+    } else {
+        __pipeline_wait_prior(0);
+    }
     __syncthreads();
     float2* a = F::template run<false>(sm, fft_scratch<F>(sm, fd), fd, tid);
+    if constexpr (STAGE) __pipeline_wait_prior(0);
     __syncthreads();
-    for (int j = tid; j < nb; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], __ldg(mrow + j));
+    for (int j = tid; j < nb; j += T) a[F::idx(j)] = cmul(a[F::idx(j)], STAGE ? ms[j] : __ldg(mrow + j));
     __syncthreads();
     a = F::template run<true>(a, a == sm ? fft_scratch<F>(sm, fd) : sm, fd, tid);
     for (int j = tid; j < n; j += T) row[j] = a[F::idx(j)];
@@ -1493,17 +1503,26 @@ void launch_rho_pass(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGe
 
 void launch_rho_pad_gen(const FftLaunch& L, dim3 grid, cudaStream_t st, const DevGeom& g, const FftDesc& fd,
                         const float2* mult_pad, float2* spec) {
-#define CALL(F) k_rho_pad_gen<F><<<grid, L.tpt, L.smem, st>>>(g, fd, mult_pad, spec)
-    LPR_FFT_SWITCH(L.variant, CALL)
+    const size_t staged = L.smem + size_t(fd.n) * sizeof(float2);
+    if (staged <= 227 * 1024) {
+#define CALL(F) k_rho_pad_gen<F, true><<<grid, L.tpt, staged, st>>>(g, fd, mult_pad, spec)
+        LPR_FFT_SWITCH(L.variant, CALL)
 #undef CALL
+    } else {
+#define CALL(F) k_rho_pad_gen<F, false><<<grid, L.tpt, L.smem, st>>>(g, fd, mult_pad, spec)
+        LPR_FFT_SWITCH(L.variant, CALL)
+#undef CALL
+    }
 }
 
-cudaError_t prepare_rho_pad_gen(const FftLaunch& L, int) {
-    const size_t bytes = L.smem;
+cudaError_t prepare_rho_pad_gen(const FftLaunch& L, int nb) {
+    const size_t staged = L.smem + size_t(nb) * sizeof(float2);
     cudaError_t e = cudaSuccess;
-#define SETG(F)                                                                          \
-    e = cudaFuncSetAttribute(k_rho_pad_gen<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             int(bytes))
+#define SETG(F)                                                                                              \
+    if (staged <= 227 * 1024)                                                                                \
+        e = cudaFuncSetAttribute(k_rho_pad_gen<F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(staged)); \
+    else                                                                                                     \
+        e = cudaFuncSetAttribute(k_rho_pad_gen<F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem))
     LPR_FFT_SWITCH(L.variant, SETG)
 #undef SETG
     return e;
