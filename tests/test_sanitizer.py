@@ -36,3 +36,22 @@ def test_compute_sanitizer(tool, cuda):
         assert re.search(r"RACECHECK SUMMARY: \d+ hazards? displayed \(0 errors", out), out[-4000:]
     else:
         assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer_bench_kernels(tool, cuda):
+    """The same tools over the kernels the bench runs (N=2048 specialisations,
+    the TMA / mbarrier rho stream, the default plan's padded rho), one slice."""
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "9"]
+    if tool == "racecheck":
+        cmd += ["--racecheck-report", "all"]
+    cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_bench_driver.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=3000)
+    out = r.stdout + r.stderr
+    print(out[-3000:])
+    assert r.returncode == 0, out[-4000:]
+    assert "sanitize driver ok" in out
+    if tool == "racecheck":
+        assert re.search(r"RACECHECK SUMMARY: \d+ hazards? displayed \(0 errors", out), out[-4000:]
+    else:
+        assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
